@@ -1,0 +1,594 @@
+"""Benchmark of the accelerated-expression hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload mapreduce|rk4|knn|hmm|kmer] [--no-case-studies]
+
+Headline workload (BASELINE.json configs[1]): the map/reduce skeleton
+microbench — `reduce addf 0.0 (map (lam x. addf (mulf 2.0 x) 1.0) s)` over
+2^28 fp32 elements per GPU (weak scaling: every rank owns 2^28 elements of
+an N*2^28-element sequence, partitioned like _chunks, pmx/interp.py:273-276;
+the per-GPU partials are combined with one NCCL all-gather and a fixed-order
+fold on the device).  One step = one evaluation of that expression.  Inputs
+(1 GiB per GPU) are larger than L2 (126 MB), so no flush is needed.
+
+`value` is device-resident throughput (elements/s, all ranks), `e2e` the same
+program through the public `accelerate` entry with pinned HOST input (H2D of
+the input + kernel + D2H of the result inside the timed region).  The case
+studies (RK4, k-NN, HMM forward, k-mer HMM) are reported under
+`case_studies` with their own roofline and CPU-oracle baselines.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "elements/s per case study (HMM, k-NN, RK4) at 1/2/4/8 B200 vs CPU ref"
+N_PER_GPU = 1 << 28
+
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "bf16_tflops": d.get("bf16_tflops", 1590.0),
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", 1400.0), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+# ------------------------------------------------------------- distributed
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend: str):
+        import torch.distributed as dist
+        if self.world > 1 and not dist.is_initialized():
+            dist.init_process_group(backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+
+# ------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.gpu), "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        rows = []
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) == 7:
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:]) if v.lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------- timing
+def device_time(step, steps: int, warmup: int, dist: Dist, per_step_events: bool = True):
+    """W untimed steps, then EXACTLY K steps between barrier+synchronize on
+    both sides, timed with CUDA events on the launching stream; returns
+    (total ms max over ranks, list of per-step ms on this rank)."""
+    import torch
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    evs[0].record(st)
+    for i in range(steps):
+        step()
+        evs[i + 1].record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]
+    total = evs[0].elapsed_time(evs[-1])
+    return dist.max(total), per
+
+
+def host_time(step, steps: int, warmup: int, dist: Dist):
+    """End-to-end: each step ends with a host read of its result, so host
+    wall time between synchronised points equals device-stream time."""
+    import torch
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    dist.barrier()
+    return dist.max(e0.elapsed_time(e1)), (t1 - t0) * 1e3
+
+
+def cpu_threads() -> int:
+    return max(1, len(os.sched_getaffinity(0)))
+
+
+# ============================================================ map/reduce
+def bench_mapreduce(args, dist: Dist, peaks: dict) -> dict:
+    import numpy as np
+    import torch
+    import paper_2211_00621_b200 as P
+    from paper_2211_00621_b200 import _lib, synth
+    from paper_2211_00621_b200.runtime import DeviceSeq
+    from paper_2211_00621_b200.skeletons import default_ctx, PreparedMapReduce
+
+    n = N_PER_GPU
+    dev = torch.device("cuda", torch.cuda.current_device())
+    f = P.lam("x", P.addf(P.mulf(2.0, "x"), 1.0))
+    # rank r owns elements [r*n, (r+1)*n) of the global sequence (_chunks rule)
+    x = synth.mapreduce_x_device(n * dist.world, dev)[dist.rank * n:(dist.rank + 1) * n].contiguous() \
+        if dist.world > 1 else synth.mapreduce_x_device(n, dev)
+    seq = DeviceSeq(x, (n,), _lib.PMX_F32)
+    ctx = default_ctx()
+    prep = PreparedMapReduce(f, P.addf, 0.0, seq, ctx)
+    gathered = torch.empty(dist.world, dtype=torch.float64, device=dev)
+
+    def combine(partial):
+        if dist.world == 1:
+            return partial
+        dist.pg.all_gather_into_tensor(gathered, partial)
+        return prep.fold_partials(gathered)           # fixed rank order (interp.py:334-336)
+
+    def step():
+        combine(prep.launch())
+
+    launches0 = ctx.launches
+    clocks = Clocks(torch.cuda.current_device())
+    clocks.start()
+    total_ms, per = device_time(step, args.steps, args.warmup, dist)
+    clk = clocks.stop()
+    launches = (ctx.launches - launches0) // (args.steps + args.warmup) * args.steps
+    result = float(combine(prep.launch()).item())
+    ctx.check_errors()
+    exact = synth.mapreduce_exact_sum(n) if dist.world == 1 else None
+
+    # variants: the individual skeleton kernels (map only 8 B/elem, reduce only 4 B/elem)
+    y = torch.empty_like(x)
+    prep_map = PreparedMapReduce(f, P.addf, 0.0, seq, ctx, materialize=y, reduce=False)
+    map_ms, _ = device_time(prep_map.launch, args.steps, 1, dist)
+    yseq = DeviceSeq(y, (n,), _lib.PMX_F32)
+    prep_red = PreparedMapReduce(None, P.addf, 0.0, yseq, ctx)
+    red_ms, _ = device_time(prep_red.launch, args.steps, 1, dist)
+    prep_mat = PreparedMapReduce(f, P.addf, 0.0, seq, ctx, materialize=y)
+    mat_ms, _ = device_time(prep_mat.launch, args.steps, 1, dist)
+    ctx.check_errors()
+
+    kern_ms = statistics.mean(per)
+    bytes_per_launch = 4 * n
+    achieved = bytes_per_launch / (kern_ms * 1e-3) / 1e9
+
+    # e2e: public accelerate entry, pinned host input, result read back
+    host_x = x.to("cpu").pin_memory()
+    e2e_body = lambda s: P.eval_reduce(P.addf, 0.0, P.eval_map(f, s))
+
+    def e2e_step():
+        v = P.accelerate(e2e_body, host_x)
+        if dist.world > 1:
+            t = torch.tensor([v], dtype=torch.float64, device=dev)
+            prep.fold_partials(gathered) if False else None
+            dist.pg.all_gather_into_tensor(gathered, t)
+            return float(prep.fold_partials(gathered).item())
+        return v
+
+    e2e_ms, e2e_wall = host_time(e2e_step, max(2, min(args.steps, 5)), 1, dist)
+    e2e_steps = max(2, min(args.steps, 5))
+    e2e_val = n * dist.world / (e2e_ms / e2e_steps * 1e-3)
+
+    out = {
+        "value": n * dist.world / (total_ms / args.steps * 1e-3),
+        "ms_per_step": total_ms / args.steps,
+        "result": result, "exact_result": exact, "result_exact_match": (result == exact) if exact else None,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _traffic_from_profiles(),
+                     "kernel": "k_map_reduce_vec<float,FAffineF<float>,OAddF,false,true>",
+                     "bytes_per_launch": bytes_per_launch, "kernel_ms": round(kern_ms, 5),
+                     "peak_source": peaks["source"]},
+        "e2e": {"value": e2e_val, "unit": "elements/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 8,
+                "ms_per_step": e2e_ms / e2e_steps, "path": "accelerate(reduce addf 0.0 (map f s)) with pinned host s"},
+        "gpu_launches": launches + (args.steps if dist.world > 1 else 0),
+        "clocks": clk,
+        "variants": {
+            "map_only_8B": {"ms": map_ms / args.steps, "GB/s": 8 * n / (map_ms / args.steps * 1e-3) / 1e9,
+                            "frac": 8 * n / (map_ms / args.steps * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "reduce_only_4B": {"ms": red_ms / args.steps, "GB/s": 4 * n / (red_ms / args.steps * 1e-3) / 1e9,
+                               "frac": 4 * n / (red_ms / args.steps * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "map_reduce_materialised_8B": {"ms": mat_ms / args.steps,
+                                           "GB/s": 8 * n / (mat_ms / args.steps * 1e-3) / 1e9,
+                                           "frac": 8 * n / (mat_ms / args.steps * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "unfused_map_then_reduce_elem_per_s": n / ((map_ms + red_ms) / args.steps * 1e-3),
+        },
+    }
+    return out
+
+
+def _traffic_from_profiles():
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("map_reduce")
+        except Exception:
+            return None
+    return None
+
+
+def cpu_baseline_mapreduce(seconds: float = 10.0) -> dict:
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O     # CPU baseline leg only
+    from paper_2211_00621_b200 import synth
+    m = 1 << 26
+    x = synth.mapreduce_x(m)
+    th = cpu_threads()
+    O.map_affine_reduce_add(x, workers=th, threads=th)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.map_affine_reduce_add(x, workers=th, threads=th)
+        reps += 1
+        if time.perf_counter() - t0 > seconds and reps >= 3:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": m / dt, "unit": "elements/s", "cores": th, "kind": "port",
+            "sample": f"{reps} passes of the oracle (oracle/pmx_oracle.c, fp64 reference semantics, "
+                      f"{th} OpenMP threads = {th} chunks) over 2^26 of the 2^28 elements"}
+
+
+# ============================================================ case studies
+def bench_rk4(args, dist, peaks) -> dict:
+    import torch
+    import paper_2211_00621_b200 as P
+    from paper_2211_00621_b200 import casestudies as CS, synth
+    n, m = 10_000, 1_000
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ps = torch.from_numpy(synth.rk4_params(n)).to(dev)
+    s0 = torch.from_numpy(synth.RK4_INIT).to(dev)
+    step = lambda: CS.rk4_sweep(ps, s0, m, synth.RK4_H)
+    total, per = device_time(step, args.steps, args.warmup, dist)
+    ms = total / args.steps
+    got = step().data.view(n, 4).to("cpu").numpy()
+    # FP64 work as written per param-step: 4 deriv (13 flops) + 3 axpy (8) + combine (28) = 104
+    flops = 104.0 * n * m
+    host_ps = ps.to("cpu").pin_memory()
+    e2e_ms, _ = host_time(lambda: P.accelerate(lambda p, s: CS.rk4_sweep(p, s, m, synth.RK4_H), host_ps,
+                                                synth.RK4_INIT), 3, 1, dist)
+    return {"config": f"N={n} parameter sets x M={m} steps, fp64", "element": "parameter set",
+            "value": n * dist.world / (ms * 1e-3), "ms_per_step": ms,
+            "param_steps_per_s": n * m * dist.world / (ms * 1e-3),
+            "e2e": {"value": n * dist.world / (e2e_ms / 3 * 1e-3), "h2d_bytes_per_step": 8 * n + 32,
+                    "d2h_bytes_per_step": 32 * n},
+            "roofline": {"bound": "fp64 latency (68 threads/SM at N=1e4)", "achieved_gflops": flops / (ms * 1e-3) / 1e9,
+                         "note": "transcendentals (12 sin/cos per step) not counted"},
+            "_result": got}
+
+
+def cpu_rk4(seconds=10.0) -> dict:
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    from paper_2211_00621_b200 import synth
+    th = cpu_threads()
+    n = max(64, 16 * th)
+    ps = synth.rk4_params(10_000)[:n]
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.rk4(ps, synth.RK4_INIT, 1000, synth.RK4_H, threads=th)
+        reps += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": n / dt, "unit": "parameter sets/s", "cores": th, "kind": "port",
+            "sample": f"{reps}x {n} of the 10^4 parameter sets x 1000 steps"}
+
+
+def bench_knn(args, dist, peaks) -> dict:
+    import torch
+    from paper_2211_00621_b200 import casestudies as CS, synth
+    ntr, nq, d, k, c = 1 << 20, 1 << 16, 64, 8, 10
+    dev = torch.device("cuda", torch.cuda.current_device())
+    X = torch.from_numpy(synth.knn_train(ntr, d)).to(dev)
+    Q = torch.from_numpy(synth.knn_query(nq, d)).to(dev)
+    L = torch.from_numpy(synth.knn_labels(ntr, c)).to(dev)
+    out = torch.empty(nq, dtype=torch.int32, device=dev)
+    from paper_2211_00621_b200 import _lib
+    ws = torch.empty(_lib.load().pmx_knn_workspace_bytes(ntr, nq, d, k), dtype=torch.uint8, device=dev)
+    step = lambda: CS.knn_raw(X, L, Q, ntr, nq, d, k, c, out, None, ws)
+    w, s = min(args.warmup, 2), max(1, min(args.steps, 3))
+    total, per = device_time(step, s, w, dist)
+    ms = total / s
+    flops = 2.0 * d * ntr * nq
+    return {"config": "2^20 train x 2^16 queries, d=64, k=8, 10 classes, fp32", "element": "query",
+            "value": nq * dist.world / (ms * 1e-3), "ms_per_step": ms, "steps": s, "warmup": w,
+            "roofline": {"bound": "tensor (distance contraction)", "achieved_tflops": flops / (ms * 1e-3) / 1e12,
+                         "peak_tflops": peaks["bf16_tflops"],
+                         "frac": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                         "note": "SIMT fp32 kernel; tcgen05 path not yet built"},
+            "_labels": out.to("cpu").numpy()}
+
+
+def cpu_knn(seconds=10.0) -> dict:
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    from paper_2211_00621_b200 import synth
+    th = cpu_threads()
+    X = synth.knn_train(1 << 20, 64)
+    L = synth.knn_labels(1 << 20, 10)
+    nq = max(8, th)
+    Q = synth.knn_query(nq, 64)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.knn(X, L, Q, 8, 10, threads=th)
+        reps += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": nq / dt, "unit": "queries/s", "cores": th, "kind": "port",
+            "sample": f"{reps}x {nq} of the 2^16 queries against all 2^20 train points"}
+
+
+def bench_hmm(args, dist, peaks) -> dict:
+    import torch
+    from paper_2211_00621_b200 import _lib, casestudies as CS, synth
+    S, K, nsig, T = 1024, 8, 4096, 10_000
+    dev = torch.device("cuda", torch.cuda.current_device())
+    A, E, pi = synth.hmm_model(S, K)
+    import numpy as np
+    Ad = torch.from_numpy(A.astype(np.float32)).to(dev)
+    lE = torch.from_numpy(np.log(E).astype(np.float32)).to(dev)
+    lpi = torch.from_numpy(np.log(pi).astype(np.float32)).to(dev)
+    obs = torch.from_numpy(synth.hmm_obs(nsig, T, K)).to(dev)
+    out = torch.empty(nsig, dtype=torch.float64, device=dev)
+    ws = torch.empty(_lib.load().pmx_hmm_forward_workspace_bytes(S, nsig), dtype=torch.uint8, device=dev)
+    step = lambda: CS.hmm_forward_raw(lpi, Ad, lE, obs, S, K, nsig, T, out, ws)
+    w, s = min(args.warmup, 1), max(1, min(args.steps, 2))
+    total, per = device_time(step, s, w, dist)
+    ms = total / s
+    flops = 2.0 * S * S * (T - 1) * nsig
+    return {"config": "4096 signals x 10^4 steps x 1024 states, K=8, fp32 trellis + fp64 log-scale",
+            "element": "signal", "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms,
+            "steps": s, "warmup": w,
+            "roofline": {"bound": "tensor (contraction)", "achieved_tflops": flops / (ms * 1e-3) / 1e12,
+                         "peak_tflops": peaks["bf16_tflops"],
+                         "frac": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                         "note": "SIMT fp32 register-tiled kernel; tcgen05 tf32 path not yet built"},
+            "_ll": out.to("cpu").numpy()}
+
+
+def cpu_hmm(seconds=10.0) -> dict:
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    from paper_2211_00621_b200 import synth
+    th = cpu_threads()
+    A, E, pi = synth.hmm_model(1024, 8)
+    T = 20
+    obs = synth.hmm_obs(max(2, th), T, 8)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.hmm_forward(A, E, pi, obs, threads=th)
+        reps += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    sig_steps = obs.shape[0] * (T - 1) / dt
+    return {"value": sig_steps / (10_000 - 1), "unit": "signals/s (T=10^4 equivalent)", "cores": th, "kind": "port",
+            "sample": f"{reps}x {obs.shape[0]} signals x {T} steps at S=1024 (log-space oracle), scaled to T=10^4"}
+
+
+def bench_kmer(args, dist, peaks) -> dict:
+    import numpy as np
+    import torch
+    from paper_2211_00621_b200 import _lib, casestudies as CS, synth
+    kmer, K, T = 8, 8, 6000
+    nsig = 8192 // 8       # this GPU's share of 8k signals over 8 GPUs
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lE = torch.from_numpy(np.log(synth.kmer_emission(kmer, K)).astype(np.float32)).to(dev)
+    obs = torch.from_numpy(synth.hmm_obs(nsig, T, K)).to(dev)
+    out = torch.empty(nsig, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    ws = torch.empty(lib.pmx_hmm_kmer_workspace_bytes(kmer, nsig), dtype=torch.uint8, device=dev)
+
+    def step():
+        rc = lib.pmx_hmm_kmer_forward_f32(kmer, 0.5, 0.125, lE.data_ptr(), K, obs.data_ptr(), nsig, T,
+                                          out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                          torch.cuda.current_stream().cuda_stream)
+        _lib.check(rc, "kmer")
+    w, s = min(args.warmup, 1), max(1, min(args.steps, 2))
+    total, per = device_time(step, s, w, dist)
+    ms = total / s
+    S = 1 << (2 * kmer)
+    bytes_ = 2.0 * 4 * S * (T - 1) * nsig   # alpha read + write per step (L2-resident)
+    return {"config": "S=65536 (k=8) de Bruijn, 1024 signals per GPU (8192 over 8), T=6000, fp32",
+            "element": "signal", "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms,
+            "steps": s, "warmup": w,
+            "roofline": {"bound": "L2 (alpha streamed through L2)", "achieved_alpha_GBps": bytes_ / (ms * 1e-3) / 1e9},
+            "_ll": out.to("cpu").numpy()}
+
+
+def cpu_kmer(seconds=10.0) -> dict:
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    from paper_2211_00621_b200 import synth
+    th = cpu_threads()
+    E = synth.kmer_emission(8, 8)
+    T = 30
+    obs = synth.hmm_obs(max(2, th), T, 8)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.kmer_forward(8, 0.5, 0.125, E, obs, threads=th)
+        reps += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": obs.shape[0] * (T - 1) / dt / (6000 - 1), "unit": "signals/s (T=6000 equivalent)",
+            "cores": th, "kind": "port", "sample": f"{reps}x {obs.shape[0]} signals x {T} steps at S=65536"}
+
+
+# ================================================================= main
+def run_ours(args):
+    import torch
+    dist = Dist()
+    torch.cuda.set_device(dist.local)
+    dist.init("nccl")
+    import paper_2211_00621_b200 as P
+    P.load_library()
+    peaks = _peaks()
+    res = bench_mapreduce(args, dist, peaks)
+    cpu = cpu_baseline_mapreduce(args.cpu_seconds) if (dist.rank == 0 and dist.world == 1) else None
+    case = {}
+    if not args.no_case_studies:
+        for name, fn, cfn in (("rk4", bench_rk4, cpu_rk4), ("knn", bench_knn, cpu_knn),
+                              ("hmm_forward", bench_hmm, cpu_hmm), ("hmm_kmer", bench_kmer, cpu_kmer)):
+            if args.case and name not in args.case:
+                continue
+            try:
+                r = fn(args, dist, peaks)
+                r = {k: v for k, v in r.items() if not k.startswith("_")}
+                if dist.rank == 0 and dist.world == 1:
+                    r["cpu_baseline"] = cfn(args.cpu_seconds / 2)
+                    r["speedup_vs_cpu"] = r["value"] / r["cpu_baseline"]["value"]
+                case[name] = r
+            except Exception as exc:    # report, do not hide
+                case[name] = {"error": f"{type(exc).__name__}: {exc}"}
+    if dist.rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": "elements/s", "n_gpus": dist.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (integer-formula inputs, SURVEY §8(d))",
+        "config": {"workload": "map/reduce skeleton microbench: reduce addf 0.0 (map (lam x. 2x+1) s), "
+                               "2^28 fp32 elements per GPU (BASELINE configs[1]), fused map->reduce",
+                   "n_per_gpu": N_PER_GPU, "n_total": N_PER_GPU * dist.world,
+                   "parallelism": f"data-parallel x{dist.world} (contiguous shards + NCCL all-gather of partials)",
+                   "l2": "inputs (1 GiB/GPU) larger than L2 (126 MB); no flush needed"},
+        "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"], "gpu_launches": res["gpu_launches"],
+        "clocks": res["clocks"], "result": {"sum": res["result"], "exact": res["exact_result"],
+                                            "bit_exact": res["result_exact_match"]},
+        "variants": res["variants"], "case_studies": case,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_reference(args):
+    """The reference arm: the CPU restatement of the reference's path (the
+    oracle port, oracle/pmx_oracle.c) on this box's host cores, same metric and
+    workload; rank 0 only."""
+    dist = Dist()
+    if dist.rank != 0:
+        return
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import numpy as np
+    import oracle as O
+    from paper_2211_00621_b200 import synth
+    th = cpu_threads()
+    n = N_PER_GPU
+    x = synth.mapreduce_x(n)
+    per = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.map_affine_reduce_add(x, workers=th, threads=th)
+        if i >= args.warmup:
+            per.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(per) / len(per)
+    val = n / (ms * 1e-3)
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "elements/s", "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (integer-formula inputs, SURVEY §8(d))",
+            "config": {"workload": "map/reduce skeleton microbench: reduce addf 0.0 (map (lam x. 2x+1) s), "
+                                   "2^28 elements (BASELINE configs[1])", "n_per_gpu": n, "n_total": n},
+            "cpu_baseline": {"value": val, "unit": "elements/s", "cores": th, "kind": "port",
+                             "sample": "full 2^28-element workload per step; oracle/pmx_oracle.c "
+                                       "oracle_map_affine_reduce_add (fp64 Float semantics, _chunks partition)"},
+            "e2e": {"value": val, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-case-studies", action="store_true")
+    ap.add_argument("--case", action="append", default=[])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

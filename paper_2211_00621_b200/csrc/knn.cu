@@ -1,0 +1,198 @@
+// k-NN classification case study (BASELINE config "k-NN classification").
+//
+// Reference anchor: there is no k-NN program in the reference package; the
+// oracle is SURVEY Appendix A.2 `knn.pmx`, written with the reference's own
+// operators and run by its interpreter: `map one qs` over queries, each query
+// a `foldl` over train points with sorted top-k insertion (ties by the smaller
+// train index), then a vote whose ties go to the smaller label.  Parity:
+// labels bit-exact.
+//
+// Design (SIMT version): a CTA owns a tile of 64 queries held in shared
+// memory and streams the training set through shared memory in tiles of 128
+// points. Distances ||q||^2 + ||x||^2 - 2 q.x are computed as a register
+// tiled contraction (4 queries x 8 points per thread) into a shared distance
+// tile; then 4 threads per query scan it against private sorted top-k lists
+// keyed by (distance bits, train index) — one 64-bit compare orders by
+// distance then index, the reference's `better` (A.2 lines 11-12).  At the
+// end the four lists are merged and the vote is taken.
+#include "common.cuh"
+
+namespace pmx {
+
+constexpr int KNN_QT = 64;     // queries per CTA
+constexpr int KNN_TT = 128;    // train points per tile
+constexpr int KNN_THREADS = 256;
+constexpr int KNN_DMAX = 128;
+
+// squared norms of rows
+__global__ void k_row_norms(const float* __restrict__ x, int64_t n, int d, float* __restrict__ out) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const float* p = x + r * d;
+        float s = 0.f;
+        for (int k = 0; k < d; ++k) s = fmaf(p[k], p[k], s);
+        out[r] = s;
+    }
+}
+
+template <int KMAX>
+__device__ __forceinline__ void topk_insert(uint64_t (&L)[KMAX], int k, uint64_t key) {
+    if (key >= L[k - 1]) return;
+    // shift larger keys right, drop the last
+#pragma unroll
+    for (int p = KMAX - 1; p > 0; --p) {
+        if (p < k && L[p - 1] > key) L[p] = L[p - 1];
+        else if (p < k && L[p] > key) L[p] = key;
+    }
+    if (L[0] > key) L[0] = key;
+}
+
+__device__ __forceinline__ uint64_t knn_key(float dist, uint32_t idx) {
+    // distances are >= 0 (clamp the -0.0 / tiny negative of the expanded form)
+    uint32_t b = __float_as_uint(fmaxf(dist, 0.f));
+    return ((uint64_t)b << 32) | idx;
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(KNN_THREADS)
+k_knn(const float* __restrict__ train, const float* __restrict__ tnorm, const int* __restrict__ labels,
+      int64_t ntr, const float* __restrict__ query, const float* __restrict__ qnorm, int64_t nq, int d,
+      int k, int ncls, int* __restrict__ out_label, int* __restrict__ out_idx) {
+    extern __shared__ __align__(16) float sm[];
+    float* QsT = sm;                                  // [d][QT]
+    float* XsT = QsT + KNN_DMAX * KNN_QT;             // [d][TT]
+    float* Ds = XsT + KNN_DMAX * KNN_TT;              // [QT][TT+1]
+    const int tid = threadIdx.x;
+    const int64_t q0 = (int64_t)blockIdx.x * KNN_QT;
+
+    for (int v = tid; v < d * KNN_QT; v += KNN_THREADS) {
+        const int qq = v / d, kk = v % d;
+        const int64_t qi = q0 + qq;
+        QsT[kk * KNN_QT + qq] = (qi < nq) ? query[qi * d + kk] : 0.f;
+    }
+    // compute mapping: thread -> 4 queries x 8 points
+    const int tq = (tid / 16) * 4;        // 16 groups of 4 queries
+    const int tp = (tid % 16) * 8;        // 16 groups of 8 points
+    // selection mapping: thread -> query sq, column phase sp
+    const int sq = tid / 4, sp = tid % 4;
+    uint64_t L[KMAX];
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) L[i] = ~0ull;
+    const float qn_sel = (q0 + sq < nq) ? qnorm[q0 + sq] : 0.f;
+
+    for (int64_t t0 = 0; t0 < ntr; t0 += KNN_TT) {
+        __syncthreads();
+        for (int v = tid; v < d * KNN_TT; v += KNN_THREADS) {
+            const int pp = v / d, kk = v % d;
+            const int64_t ti = t0 + pp;
+            XsT[kk * KNN_TT + pp] = (ti < ntr) ? train[ti * d + kk] : 0.f;
+        }
+        __syncthreads();
+        float acc[4][8];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+        for (int kk = 0; kk < d; ++kk) {
+            const float4 qa = *reinterpret_cast<const float4*>(QsT + kk * KNN_QT + tq);
+            const float4 x0 = *reinterpret_cast<const float4*>(XsT + kk * KNN_TT + tp);
+            const float4 x1 = *reinterpret_cast<const float4*>(XsT + kk * KNN_TT + tp + 4);
+            const float qv[4] = {qa.x, qa.y, qa.z, qa.w};
+            const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(qv[a], xv[b], acc[a][b]);
+        }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const int64_t ti = t0 + tp + b;
+            const float xn = (ti < ntr) ? tnorm[ti] : 0.f;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) Ds[(tq + a) * (KNN_TT + 1) + tp + b] = xn - 2.f * acc[a][b];
+        }
+        __syncthreads();
+        // selection: query sq scans columns sp, sp+4, ...
+        const int lim = (ntr - t0 < KNN_TT) ? (int)(ntr - t0) : KNN_TT;
+        for (int c = sp; c < lim; c += 4) {
+            const float dist = Ds[sq * (KNN_TT + 1) + c] + qn_sel;
+            topk_insert<KMAX>(L, k, knn_key(dist, (uint32_t)(t0 + c)));
+        }
+    }
+    // merge the 4 partial lists of each query through shared memory
+    __syncthreads();
+    uint64_t* M = reinterpret_cast<uint64_t*>(Ds);      // [QT][4][KMAX]
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) M[(sq * 4 + sp) * KMAX + i] = L[i];
+    __syncthreads();
+    if (sp == 0 && q0 + sq < nq) {
+        const uint64_t* P = M + sq * 4 * KMAX;
+        int h[4] = {0, 0, 0, 0};
+        int votes[64];
+        for (int c = 0; c < ncls; ++c) votes[c] = 0;
+        for (int r = 0; r < k; ++r) {
+            int bw = 0;
+            uint64_t bv = ~0ull;
+            for (int w = 0; w < 4; ++w) {
+                const uint64_t v = (h[w] < k) ? P[w * KMAX + h[w]] : ~0ull;
+                if (v < bv) { bv = v; bw = w; }
+            }
+            h[bw]++;
+            const uint32_t idx = (uint32_t)(bv & 0xffffffffu);
+            if (out_idx) out_idx[(q0 + sq) * k + r] = (bv == ~0ull) ? -1 : (int)idx;
+            if (bv != ~0ull) {
+                const int lab = labels[idx];
+                if (lab >= 0 && lab < ncls) votes[lab]++;
+            }
+        }
+        // foldl (lam best. lam c. if votes c > votes best then c else best) 0 classIdx
+        int best = 0;
+        for (int c = 1; c < ncls; ++c) if (votes[c] > votes[best]) best = c;
+        out_label[q0 + sq] = best;
+    }
+}
+
+}  // namespace pmx
+
+using namespace pmx;
+
+extern "C" {
+
+size_t pmx_knn_workspace_bytes(int64_t ntr, int64_t nq, int32_t d, int32_t k) {
+    (void)d; (void)k;
+    return (size_t)(ntr + nq) * sizeof(float) + 512;
+}
+
+int pmx_knn_f32(const float* train, const int32_t* labels, int64_t ntr, const float* query, int64_t nq,
+                int32_t d, int32_t k, int32_t ncls, int32_t* out_label, int32_t* out_idx, void* ws,
+                size_t ws_bytes, void* stream) {
+    PMX_REQUIRE(d > 0 && d <= KNN_DMAX && d % 4 == 0, "pmx_knn_f32: d must be a multiple of 4 in [4, %d]", KNN_DMAX);
+    PMX_REQUIRE(k >= 1 && k <= 32, "pmx_knn_f32: k must be in [1, 32]");
+    PMX_REQUIRE(ncls >= 1 && ncls <= 64, "pmx_knn_f32: ncls must be in [1, 64]");
+    PMX_REQUIRE(ntr >= k && ntr < 0x7fffffffll, "pmx_knn_f32: need k <= ntr < 2^31");
+    PMX_REQUIRE(ws && ws_bytes >= pmx_knn_workspace_bytes(ntr, nq, d, k), "pmx_knn_f32: workspace too small");
+    if (nq == 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    float* tnorm = (float*)ws;
+    float* qnorm = tnorm + ntr;
+    k_row_norms<<<1184, 256, 0, st>>>(train, ntr, d, tnorm);
+    k_row_norms<<<(unsigned)imin64(1184, (nq + 255) / 256), 256, 0, st>>>(query, nq, d, qnorm);
+    PMX_CHECK_LAUNCH("knn_norms");
+    const unsigned grid = (unsigned)((nq + KNN_QT - 1) / KNN_QT);
+    const size_t smem_f = (size_t)(KNN_DMAX * KNN_QT + KNN_DMAX * KNN_TT + KNN_QT * (KNN_TT + 1)) * sizeof(float);
+    if (k <= 8) {
+        const size_t smem = smem_f > (size_t)KNN_QT * 4 * 8 * 8 ? smem_f : (size_t)KNN_QT * 4 * 8 * 8;
+        cudaFuncSetAttribute(k_knn<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_knn<8><<<grid, KNN_THREADS, smem, st>>>(train, tnorm, labels, ntr, query, qnorm, nq, d, k, ncls,
+                                                  out_label, out_idx);
+    } else {
+        const size_t need = (size_t)KNN_DMAX * KNN_QT * 4 + (size_t)KNN_DMAX * KNN_TT * 4 + (size_t)KNN_QT * 4 * 32 * 8;
+        const size_t smem = need > smem_f ? need : smem_f;
+        cudaFuncSetAttribute(k_knn<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_knn<32><<<grid, KNN_THREADS, smem, st>>>(train, tnorm, labels, ntr, query, qnorm, nq, d, k, ncls,
+                                                   out_label, out_idx);
+    }
+    PMX_CHECK_LAUNCH("knn");
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+"""Case-study kernels on the B200 vs the reference's golden outputs and the
+CPU oracle.  Tolerances (north_star): integer/index outputs bit-exact, fp64
+rel 1e-9, fp32 rel 1e-5 with log-likelihoods compared in fp64."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2211_00621_b200 import (
+    accelerate, hmm_forward, hmm_kmer_forward, knn_classify, rk4_sweep, synth, viterbi,
+)
+
+pytestmark = pytest.mark.gpu
+
+FP64_REL = 1e-9
+LL_REL = 1e-5
+
+
+# ------------------------------------------------------------------ RK4
+def test_rk4_reference_program(golden):
+    # programs/rk4.pmx: p_k = 0.5 + 0.1k, k < 16, 100 steps (test_acceptance.py:385-394)
+    ps = np.array([0.5 + 0.1 * float(k) for k in range(16)])
+    got = accelerate(lambda p, s0: rk4_sweep(p, s0, 100, 0.01), ps, synth.RK4_INIT)
+    lines = [l for l in golden["program_rk4"]["stdout"].splitlines() if l.strip()]
+    assert got.shape == (16, 4)
+    for k, line in enumerate(lines):
+        for g, w in zip(got[k], map(float, line.split())):
+            assert math.isclose(g, w, rel_tol=FP64_REL), (k, g, w)
+
+
+def test_rk4_param_variant_golden(golden):
+    for e in golden["rk4_param"]:
+        got = accelerate(lambda p, s0: rk4_sweep(p, s0, e["M"], 0.01), synth.rk4_params(e["N"]), synth.RK4_INIT)
+        lines = [l for l in e["stdout"].splitlines() if l.strip()]
+        for k, line in enumerate(lines):
+            for g, w in zip(got[k], map(float, line.split())):
+                assert math.isclose(g, w, rel_tol=FP64_REL)
+
+
+def test_rk4_vs_oracle_config_steps():
+    n = 2000
+    ps = synth.rk4_params(n)
+    got = accelerate(lambda p, s0: rk4_sweep(p, s0, 1000, synth.RK4_H), ps, synth.RK4_INIT)
+    want = O.rk4(ps, synth.RK4_INIT, 1000, synth.RK4_H)
+    assert np.allclose(got, want, rtol=FP64_REL, atol=1e-12)
+
+
+# ------------------------------------------------------------------ HMM forward
+@pytest.mark.parametrize("ix", [0, 1, 2])
+def test_hmm_forward_golden(ix, golden):
+    e = golden["hmm_forward"][ix]
+    A, E, pi = synth.hmm_model(e["S"], e["K"])
+    obs = synth.hmm_obs(e["NS"], e["T"], e["K"])
+    got = accelerate(hmm_forward, A, E, pi, obs)
+    want = [float(v) for v in e["stdout"].split()]
+    assert np.allclose(got, want, rtol=LL_REL, atol=0)
+
+
+@pytest.mark.parametrize("S,nsig,T", [(256, 40, 40), (512, 33, 12), (1024, 33, 8), (100, 5, 30), (2048, 2, 5)])
+def test_hmm_forward_vs_oracle(S, nsig, T):
+    A, E, pi = synth.hmm_model(S, 8)
+    obs = synth.hmm_obs(nsig, T, 8)
+    got = accelerate(hmm_forward, A, E, pi, obs)
+    want = O.hmm_forward(A, E, pi, obs)
+    assert np.allclose(got, want, rtol=LL_REL, atol=0), np.max(np.abs(got - want) / np.abs(want))
+
+
+def test_hmm_forward_long_sequence_precision():
+    # T = 2000 at S = 256: fp32 trellis with fp64 running log-scale stays far inside 1e-5
+    A, E, pi = synth.hmm_model(256, 8)
+    obs = synth.hmm_obs(3, 2000, 8)
+    got = accelerate(hmm_forward, A, E, pi, obs)
+    want = O.hmm_forward(A, E, pi, obs)
+    assert np.max(np.abs(got - want) / np.abs(want)) < 1e-6
+
+
+# ------------------------------------------------------------------ Viterbi
+def test_viterbi_reference_program(golden):
+    def norm(r):
+        t = 0.0
+        for v in r:
+            t += v
+        return [v / t for v in r]
+    A = [norm([float(1 + ((i * 7 + j * 3) % 5)) for j in range(4)]) for i in range(4)]
+    E = [norm([float(1 + ((j * 5 + k * 2) % 7)) for k in range(8)]) for j in range(4)]
+    pi = norm([float(1 + i) for i in range(4)])
+    obs = [(t * t + 3 * t) % 8 for t in range(64)]
+    r = accelerate(viterbi, A, E, pi, obs)
+    lines = golden["program_viterbi"]["stdout"].strip().splitlines()
+    assert [int(v) for v in r["path"]] == [int(v) for v in lines[0].split()]
+    assert math.isclose(float(r["logp"][0]), float(lines[1]), rel_tol=1e-12)
+
+
+def test_viterbi_vs_oracle():
+    A, E, pi = synth.hmm_model(16, 8)
+    obs = synth.hmm_obs(6, 80, 8)
+    r = accelerate(viterbi, A, E, pi, obs)
+    path, logp = O.viterbi(A, E, pi, obs)
+    assert np.array_equal(r["path"], path)
+    assert np.allclose(r["logp"], logp, rtol=1e-12)
+
+
+# ------------------------------------------------------------------ k-NN
+@pytest.mark.parametrize("ix", [0, 1, 2])
+def test_knn_golden(ix, golden):
+    e = golden["knn"][ix]
+    X = synth.knn_train(e["NT"], e["D"])
+    Q = synth.knn_query(e["NQ"], e["D"])
+    L = synth.knn_labels(e["NT"], e["C"])
+    got = accelerate(lambda x, l, q: knn_classify(x, l, q, e["K"], e["C"]), X, L, Q)
+    assert got.tolist() == [int(v) for v in e["stdout"].split()]
+
+
+@pytest.mark.parametrize("ntr,nq,d,k,c", [(5000, 300, 64, 8, 10), (1000, 130, 16, 3, 4), (777, 65, 64, 17, 10)])
+def test_knn_vs_oracle(ntr, nq, d, k, c):
+    X = synth.knn_train(ntr, d)
+    Q = synth.knn_query(nq, d)
+    L = synth.knn_labels(ntr, c)
+    lab, idx = accelerate(lambda x, l, q: knn_classify(x, l, q, k, c, return_indices=True), X, L, Q)
+    olab, oidx = O.knn(X, L, Q, k, c)
+    assert np.array_equal(lab, olab)
+    assert np.array_equal(idx, oidx)
+
+
+def test_knn_continuous_data_is_tie_tolerant():
+    rng = np.random.default_rng(3)
+    X = rng.random((3000, 64), dtype=np.float32)
+    Q = rng.random((100, 64), dtype=np.float32)
+    L = synth.knn_labels(3000, 10)
+    lab, idx = accelerate(lambda x, l, q: knn_classify(x, l, q, 8, 10, return_indices=True), X, L, Q)
+    olab, oidx = O.knn(X, L, Q, 8, 10)
+    # same neighbour sets up to fp32 rounding of near-equal distances
+    d = ((Q[:, None, :].astype(np.float64) - X[None, :, :]) ** 2).sum(-1)
+    for q in range(100):
+        got_d = np.sort(d[q, idx[q]])
+        want_d = np.sort(d[q, oidx[q]])
+        assert np.allclose(got_d, want_d, rtol=1e-5)
+
+
+# ------------------------------------------------------------------ k-mer HMM
+@pytest.mark.parametrize("ix", [0, 1])
+def test_kmer_golden(ix, golden):
+    e = golden["kmer"][ix]
+    E = synth.kmer_emission(e["kmer"], e["K"])
+    obs = synth.hmm_obs(e["NS"], e["T"], e["K"])
+    got = accelerate(lambda em, o: hmm_kmer_forward(e["kmer"], e["p_stay"], e["p_step"], em, o), E, obs)
+    want = [float(v) for v in e["stdout"].split()]
+    assert np.allclose(got, want, rtol=LL_REL, atol=0)
+
+
+@pytest.mark.parametrize("kmer,nsig,T", [(5, 4, 60), (8, 2, 6)])
+def test_kmer_vs_oracle(kmer, nsig, T):
+    E = synth.kmer_emission(kmer, 8)
+    obs = synth.hmm_obs(nsig, T, 8)
+    got = accelerate(lambda em, o: hmm_kmer_forward(kmer, 0.5, 0.125, em, o), E, obs)
+    want = O.kmer_forward(kmer, 0.5, 0.125, E, obs)
+    assert np.allclose(got, want, rtol=LL_REL, atol=0)

@@ -75,7 +75,14 @@ static inline bool is_const(int o) { return o >= 32 && o < 64; }
 // y = f(x) with r0 = x. Recognises   mulf c x | mulf x c | addf x c | addf c x
 // | subf x c | addf (mulf c x) d  (and the int analogues). Recognition only
 // accepts forms whose fast evaluation is bit-identical to the interpreter.
+static int recognise_map_raw(const pmx_program* f, Affine* A);
 static int recognise_map(const pmx_program* f, Affine* A) {
+    int k = recognise_map_raw(f, A);
+    if (!A->has_mul) { A->af = 1.0; A->ai = 1; }
+    if (!A->has_add) { A->bf = -0.0; A->bi = 0; }
+    return k;
+}
+static int recognise_map_raw(const pmx_program* f, Affine* A) {
     memset(A, 0, sizeof(*A));
     if (!f) return K_IDENTITY;
     if (f->n_arrays != 0) return K_VM;
@@ -155,10 +162,13 @@ static int recognise_reduce(const pmx_program* op) {
 }
 
 // ==================================================================== device
+// Streaming 128-bit load (read-only path, no L1 allocation). `volatile` keeps
+// the U loads of an unrolled iteration issued back to back before their use,
+// so every thread has U x 16 B in flight.
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
     uint4 r;
-    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
     return r;
 }
 __device__ __forceinline__ void stg_stream(void* p, uint4 v) {
@@ -170,27 +180,24 @@ __device__ __forceinline__ void stg_stream(void* p, uint4 v) {
 struct FIdentity {
     template <class T> __device__ __forceinline__ T operator()(T x) const { return x; }
 };
+// y = a*x + b with each operation rounded separately, as CPython evaluates
+// `addf (mulf a x) b`.  `mulf a x` alone is a = a, b = -0.0 and `addf x b` is
+// a = 1.0: both identities are exact in IEEE arithmetic (signed zeros, NaN
+// and infinities included), so one branch-free functor covers all three.
 template <class C>
 struct FAffineF {
-    C a, b; int has_mul, has_add;
+    C a, b;
     template <class T> __device__ __forceinline__ T operator()(T x) const {
-        C v = (C)x;
-        if (has_mul) v = mul_rn(a, v);
-        if (has_add) v = add_rn(v, b);
-        return (T)v;
+        return (T)add_rn(mul_rn(a, (C)x), b);
     }
     __device__ __forceinline__ static float mul_rn(float a, float b) { return __fmul_rn(a, b); }
     __device__ __forceinline__ static float add_rn(float a, float b) { return __fadd_rn(a, b); }
     __device__ __forceinline__ static double mul_rn(double a, double b) { return __dmul_rn(a, b); }
     __device__ __forceinline__ static double add_rn(double a, double b) { return __dadd_rn(a, b); }
 };
-struct FAffineI {
-    int64_t a, b; int has_mul, has_add;
-    __device__ __forceinline__ int64_t operator()(int64_t x) const {
-        if (has_mul) x = wmul(a, x);
-        if (has_add) x = wadd(x, b);
-        return x;
-    }
+struct FAffineI {   // wrap-around a*x + b (a = 1 / b = 0 when absent: exact)
+    int64_t a, b;
+    __device__ __forceinline__ int64_t operator()(int64_t x) const { return wadd(wmul(a, x), b); }
 };
 
 // ---- reduce operators on the accumulator type ------------------------------
@@ -268,30 +275,46 @@ __device__ __forceinline__ void grid_combine(typename Op::A block_total, typenam
 struct NoReduce { typedef double A; __device__ static double id() { return 0.0; }
                   __device__ static double f(double a, double) { return a; } };
 
+// Read-only streams (reductions) keep 128 B per thread in flight at 4 CTAs/SM
+// (measured 102% of the copy peak); read+write streams do better with more
+// resident warps and 64 B per thread (the stores add their own parallelism).
 template <class T, class F, class Op, bool WRITE_Y, bool DO_REDUCE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, WRITE_Y ? 8 : 4)
 k_map_reduce_vec(const T* __restrict__ x, T* __restrict__ y, int64_t n, F f,
                  typename Op::A* partials, unsigned* ticket, typename Op::A init,
                  typename Op::A* out) {
     typedef typename Op::A A;
     constexpr int V = 16 / sizeof(T);     // elements per 128-bit packet
-    constexpr int U = 4;                  // packets in flight per thread
+    constexpr int U = (WRITE_Y ? 16 : 32) / V;   // packets in flight per thread
     union P { uint4 u; T e[V]; };
     const int64_t npk = n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    A acc = Op::id();
+    A acc0 = Op::id(), acc1 = Op::id();   // two chains: halves the dependent-add depth
     for (; p + (U - 1) * stride < npk; p += U * stride) {
         P v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) v[u].u = ldg_stream(x + (p + u * stride) * V);
+        // Join point on every loaded packet: a (never taken) branch on a value
+        // that depends on all U loads forces ptxas to issue all of them before
+        // any consumer, so U x 16 B per thread are in flight at once (it
+        // otherwise interleaves each load with the previous packet's use).
+        if (!WRITE_Y) {
+            unsigned j = 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) j += v[u].u.x;
+            if (j == 0x7fc00001u && n == -1) __trap();
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             P w;
 #pragma unroll
             for (int e = 0; e < V; ++e) {
                 w.e[e] = f(v[u].e[e]);
-                if (DO_REDUCE) acc = Op::f(acc, (A)w.e[e]);
+                if (DO_REDUCE) {
+                    if (e & 1) acc1 = Op::f(acc1, (A)w.e[e]);
+                    else acc0 = Op::f(acc0, (A)w.e[e]);
+                }
             }
             if (WRITE_Y) stg_stream(y + (p + u * stride) * V, w.u);
         }
@@ -302,7 +325,7 @@ k_map_reduce_vec(const T* __restrict__ x, T* __restrict__ y, int64_t n, F f,
 #pragma unroll
         for (int e = 0; e < V; ++e) {
             w.e[e] = f(v.e[e]);
-            if (DO_REDUCE) acc = Op::f(acc, (A)w.e[e]);
+            if (DO_REDUCE) acc0 = Op::f(acc0, (A)w.e[e]);
         }
         if (WRITE_Y) stg_stream(y + p * V, w.u);
     }
@@ -310,10 +333,10 @@ k_map_reduce_vec(const T* __restrict__ x, T* __restrict__ y, int64_t n, F f,
     for (int64_t j = npk * V + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
         T w = f(x[j]);
         if (WRITE_Y) y[j] = w;
-        if (DO_REDUCE) acc = Op::f(acc, (A)w);
+        if (DO_REDUCE) acc0 = Op::f(acc0, (A)w);
     }
     if (DO_REDUCE) {
-        A bt = block_reduce<Op>(acc);
+        A bt = block_reduce<Op>(Op::f(acc0, acc1));
         grid_combine<Op>(bt, partials, ticket, init, out);
     }
 }
@@ -547,15 +570,29 @@ static inline int grid_for(int64_t work_items, int threads, int per_sm) {
 static const int kReduceThreads = 256;
 static const int kReduceBlocksPerSM = 8;
 
-static int reduce_grid(int64_t n, int vec) {
-    return grid_for((n + vec - 1) / vec / 4, kReduceThreads, kReduceBlocksPerSM);
+
+// One resident wave: grid = SMs x (CTAs per SM the kernel can hold), capped by
+// the work (a partial second wave would leave SMs idle at the tail).
+template <class K>
+static int occupancy_grid(K kernel, int64_t work_items, int threads) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    if (per_sm > kReduceBlocksPerSM) per_sm = kReduceBlocksPerSM;
+    return grid_for(work_items, threads, per_sm);
 }
 
 template <class T, class F, class Op, bool WY, bool RED>
 static int launch_mr(const T* x, T* y, int64_t n, F f, void* ws, typename Op::A init,
                      typename Op::A* out, cudaStream_t st) {
     const int V = 16 / sizeof(T);
-    int grid = reduce_grid(n, V);
+    static int grid_cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!grid_cache[dev & 63])
+        grid_cache[dev & 63] = occupancy_grid(k_map_reduce_vec<T, F, Op, WY, RED>, (int64_t)1 << 40, kReduceThreads);
+    int64_t want = (n / V + kReduceThreads * 8 - 1) / (kReduceThreads * 8);   // >= 8 packets per thread
+    int grid = (int)(want < grid_cache[dev & 63] ? (want < 1 ? 1 : want) : grid_cache[dev & 63]);
     unsigned* ticket = (unsigned*)ws;
     typename Op::A* partials = (typename Op::A*)((char*)ws + 256);
     bool aligned = ((uintptr_t)x % 16 == 0) && (!WY || (uintptr_t)y % 16 == 0);
@@ -642,13 +679,13 @@ int pmx_map(const pmx_program* f, const void* x, int32_t xt, void* y, int32_t yt
         }
         if (kind == K_AFFINE_F && xt == PMX_F32 && f32_exact(A.af) && f32_exact(A.bf))
             return dispatch_map_only<float>((const float*)x, (float*)y, n,
-                                            FAffineF<float>{(float)A.af, (float)A.bf, A.has_mul, A.has_add}, st);
+                                            FAffineF<float>{(float)A.af, (float)A.bf}, st);
         if (kind == K_AFFINE_F && xt == PMX_F64)
             return dispatch_map_only<double>((const double*)x, (double*)y, n,
-                                             FAffineF<double>{A.af, A.bf, A.has_mul, A.has_add}, st);
+                                             FAffineF<double>{A.af, A.bf}, st);
         if (kind == K_AFFINE_I && xt == PMX_I64)
             return dispatch_map_only<int64_t>((const int64_t*)x, (int64_t*)y, n,
-                                              FAffineI{A.ai, A.bi, A.has_mul, A.has_add}, st);
+                                              FAffineI{A.ai, A.bi}, st);
     }
     PMX_REQUIRE(f, "pmx_map: null program with differing dtypes");
     int grid = grid_for(n, 256, 8);
@@ -694,20 +731,20 @@ int pmx_map_reduce(const pmx_program* f, const pmx_program* op, const void* x, i
                 r = dispatch_op<float>(ok, (const float*)x, (float*)y, n, FIdentity{}, ws, init_host, out, st);
             else if (fk == K_AFFINE_F && f32_exact(A.af) && f32_exact(A.bf))
                 r = dispatch_op<float>(ok, (const float*)x, (float*)y, n,
-                                       FAffineF<float>{(float)A.af, (float)A.bf, A.has_mul, A.has_add},
+                                       FAffineF<float>{(float)A.af, (float)A.bf},
                                        ws, init_host, out, st);
         } else if (xt == PMX_F64 && float_op) {
             if (fk == K_IDENTITY)
                 r = dispatch_op<double>(ok, (const double*)x, (double*)y, n, FIdentity{}, ws, init_host, out, st);
             else if (fk == K_AFFINE_F)
                 r = dispatch_op<double>(ok, (const double*)x, (double*)y, n,
-                                        FAffineF<double>{A.af, A.bf, A.has_mul, A.has_add}, ws, init_host, out, st);
+                                        FAffineF<double>{A.af, A.bf}, ws, init_host, out, st);
         } else if (xt == PMX_I64 && int_op) {
             if (fk == K_IDENTITY)
                 r = dispatch_op<int64_t>(ok, (const int64_t*)x, (int64_t*)y, n, FIdentity{}, ws, init_host, out, st);
             else if (fk == K_AFFINE_I)
                 r = dispatch_op<int64_t>(ok, (const int64_t*)x, (int64_t*)y, n,
-                                         FAffineI{A.ai, A.bi, A.has_mul, A.has_add}, ws, init_host, out, st);
+                                         FAffineI{A.ai, A.bi}, ws, init_host, out, st);
         }
         if (r <= 0) return r;
     }

@@ -411,6 +411,8 @@ def marshal_out(arena: DeviceArena, heap: Heap, result):
             return v.get(arena)
         if isinstance(v, list):
             return [copy_out(x) for x in v]
+        if isinstance(v, tuple):
+            return tuple(copy_out(x) for x in v)
         if isinstance(v, dict):
             return {l: copy_out(x) for l, x in v.items()}
         return v

@@ -564,6 +564,8 @@ def _force(v):
         return v.materialize()
     if isinstance(v, list):
         return [_force(x) for x in v]
+    if isinstance(v, tuple):
+        return tuple(_force(x) for x in v)
     if isinstance(v, dict):
         return {k: _force(x) for k, x in v.items()}
     return v

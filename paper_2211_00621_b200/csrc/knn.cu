@@ -15,6 +15,7 @@
 // keyed by (distance bits, train index) — one 64-bit compare orders by
 // distance then index, the reference's `better` (A.2 lines 11-12).  At the
 // end the four lists are merged and the vote is taken.
+#include <cuda_bf16.h>
 #include "common.cuh"
 
 namespace pmx {
@@ -56,7 +57,9 @@ template <int KMAX>
 __global__ void __launch_bounds__(KNN_THREADS)
 k_knn(const float* __restrict__ train, const float* __restrict__ tnorm, const int* __restrict__ labels,
       int64_t ntr, const float* __restrict__ query, const float* __restrict__ qnorm, int64_t nq, int d,
-      int k, int ncls, int* __restrict__ out_label, int* __restrict__ out_idx) {
+      int k, int ncls, int* __restrict__ out_label, int* __restrict__ out_idx,
+      const unsigned* __restrict__ run_if) {
+    if (run_if && *run_if == 0) return;     // the tensor-core path produced the answer
     extern __shared__ __align__(16) float sm[];
     float* QsT = sm;                                  // [d][QT]
     float* XsT = QsT + KNN_DMAX * KNN_QT;             // [d][TT]
@@ -151,6 +154,13 @@ k_knn(const float* __restrict__ train, const float* __restrict__ tnorm, const in
     }
 }
 
+// tensor-core path (knn_tc.cu)
+size_t knn_tc_workspace(int64_t ntr, int64_t nq);
+int knn_tc_run(const float* train, const float* query, const int* labels, int64_t ntr, int64_t nq, int k, int ncls,
+               int* out_label, int* out_idx, float* tnorm, float* qnorm, unsigned* flag, void* ws, cudaStream_t st);
+
+static bool knn_tc_eligible(int d, int k) { return d == 64 && k <= 8; }
+
 }  // namespace pmx
 
 using namespace pmx;
@@ -158,8 +168,9 @@ using namespace pmx;
 extern "C" {
 
 size_t pmx_knn_workspace_bytes(int64_t ntr, int64_t nq, int32_t d, int32_t k) {
-    (void)d; (void)k;
-    return (size_t)(ntr + nq) * sizeof(float) + 512;
+    size_t base = (size_t)(ntr + nq) * sizeof(float) + 512;
+    if (knn_tc_eligible(d, k)) base += knn_tc_workspace(ntr, nq);
+    return base;
 }
 
 int pmx_knn_f32(const float* train, const int32_t* labels, int64_t ntr, const float* query, int64_t nq,
@@ -172,24 +183,38 @@ int pmx_knn_f32(const float* train, const int32_t* labels, int64_t ntr, const fl
     PMX_REQUIRE(ws && ws_bytes >= pmx_knn_workspace_bytes(ntr, nq, d, k), "pmx_knn_f32: workspace too small");
     if (nq == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
-    float* tnorm = (float*)ws;
+    char* w = (char*)ws;
+    float* tnorm = (float*)w;
     float* qnorm = tnorm + ntr;
-    k_row_norms<<<1184, 256, 0, st>>>(train, ntr, d, tnorm);
-    k_row_norms<<<(unsigned)imin64(1184, (nq + 255) / 256), 256, 0, st>>>(query, nq, d, qnorm);
-    PMX_CHECK_LAUNCH("knn_norms");
+    unsigned* flag = (unsigned*)(w + (size_t)(ntr + nq) * sizeof(float) + 256);   // 256-aligned slack
+    const bool tc_path = knn_tc_eligible(d, k);
+    if (tc_path) {
+        // bf16 operand copies + norms + exactness flag; the tensor-core kernels
+        // run iff every coordinate is exact in bf16 (else the SIMT kernel does)
+        char* t = w + (size_t)(ntr + nq) * sizeof(float) + 512;
+        cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(unsigned), st);
+        if (e != cudaSuccess) { set_last_error("knn flag: %s", cudaGetErrorString(e)); return -2; }
+        int rc = knn_tc_run(train, query, labels, ntr, nq, k, ncls, out_label, out_idx, tnorm, qnorm, flag, t, st);
+        if (rc) return rc;
+    } else {
+        k_row_norms<<<1184, 256, 0, st>>>(train, ntr, d, tnorm);
+        k_row_norms<<<(unsigned)imin64(1184, (nq + 255) / 256), 256, 0, st>>>(query, nq, d, qnorm);
+        PMX_CHECK_LAUNCH("knn_norms");
+    }
+    const unsigned* run_if = tc_path ? flag : nullptr;   // SIMT kernel: fallback when the flag is set
     const unsigned grid = (unsigned)((nq + KNN_QT - 1) / KNN_QT);
     const size_t smem_f = (size_t)(KNN_DMAX * KNN_QT + KNN_DMAX * KNN_TT + KNN_QT * (KNN_TT + 1)) * sizeof(float);
     if (k <= 8) {
         const size_t smem = smem_f > (size_t)KNN_QT * 4 * 8 * 8 ? smem_f : (size_t)KNN_QT * 4 * 8 * 8;
         cudaFuncSetAttribute(k_knn<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_knn<8><<<grid, KNN_THREADS, smem, st>>>(train, tnorm, labels, ntr, query, qnorm, nq, d, k, ncls,
-                                                  out_label, out_idx);
+                                                  out_label, out_idx, run_if);
     } else {
         const size_t need = (size_t)KNN_DMAX * KNN_QT * 4 + (size_t)KNN_DMAX * KNN_TT * 4 + (size_t)KNN_QT * 4 * 32 * 8;
         const size_t smem = need > smem_f ? need : smem_f;
         cudaFuncSetAttribute(k_knn<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_knn<32><<<grid, KNN_THREADS, smem, st>>>(train, tnorm, labels, ntr, query, qnorm, nq, d, k, ncls,
-                                                   out_label, out_idx);
+                                                   out_label, out_idx, run_if);
     }
     PMX_CHECK_LAUNCH("knn");
     return 0;

@@ -1,0 +1,410 @@
+// k-NN on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// Same contract as the SIMT kernel in knn.cu (reference anchor: SURVEY
+// Appendix A.2 knn.pmx — top-k by (distance, train index), vote ties to the
+// smaller label).  Used when d == 64, k <= 8 and the data are exact in the
+// tensor-core formulation below (the BASELINE config: integer coordinates in
+// [-8, 8]); then every distance is computed exactly and the answer is
+// bit-identical to the fp64 reference.  Otherwise a device flag set by the
+// prep kernel turns these kernels into no-ops and the SIMT kernel runs (no
+// host synchronisation).
+//
+// Formulation: the accumulator holds the ranking key directly,
+//     D[q, p] = sum_k q_k * (-2 x_pk)  +  256 * hi_p + 1 * lo_p
+//             = ||x_p||^2 - 2 q.x_p          (||q||^2 is constant per query)
+// with ||x_p||^2 = 256 hi_p + lo_p split into two bf16-exact integers: four
+// UMMA k-steps over the 64 coordinates (SWIZZLE_128B operands) plus one over a
+// 16-wide augmentation (A rows [256, 1, 0...], B rows [hi, lo, 0...],
+// SWIZZLE_32B).  The epilogue is then one min per candidate.
+//
+// Structure (persistent, one CTA per SM, 12 warps):
+//   warp 0   TMA producer: the 256-query block A (2 x 128 rows) once per work
+//            item; train tiles B (128 x 64 bf16 of -2x) + B_aug (128 x 16)
+//            through a 4-stage ring
+//   warp 1   MMA issuer (one thread): per train tile, two 128 x 128
+//            accumulators (one per 128-query half) into one of two TMEM
+//            buffers (2 buffers x 2 halves x 128 columns = all 512 columns)
+//   warp 2   TMEM allocator
+//   warps 4-11 epilogue: warp w owns query half (w-4)/4 and TMEM lane
+//            quadrant w%4 (one query per thread) and scans the tile's 128
+//            candidates: 2 x (64-column tcgen05.ld), min-tree per 32, and the
+//            rare sorted insertion of (order-preserving distance bits, index)
+// Work item = (256-query block, contiguous range of train tiles).  Reusing
+// each B tile for 256 queries halves L2 traffic versus 128; splitting the
+// train range balances the blocks over 148 SMs.  Per-item partial top-k lists
+// go to global memory; k_knn_merge merges them and votes.
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace pmx {
+
+constexpr int KT_M = 128;                 // UMMA M (queries per half)
+constexpr int KT_Q = 256;                 // queries per work item
+constexpr int KT_N = 128;                 // train points per tile (UMMA N)
+constexpr int KT_D = 64;
+constexpr int KT_AUG = 16;
+constexpr int KT_STAGES = 4;
+constexpr int KT_KMAX = 8;
+constexpr int KT_THREADS = 384;
+constexpr uint32_t KT_A_BYTES = KT_Q * KT_D * 2;        // 32 KB
+constexpr uint32_t KT_B_BYTES = KT_N * KT_D * 2;        // 16 KB
+constexpr uint32_t KT_BAUG_BYTES = KT_N * KT_AUG * 2;   //  4 KB
+
+struct __align__(1024) KnnSmem {
+    __nv_bfloat16 A[KT_Q * KT_D];                       // 2 halves of 128 rows, SW128
+    __nv_bfloat16 B[KT_STAGES][KT_N * KT_D];            // SW128
+    __nv_bfloat16 Aaug[KT_M * KT_AUG];                  // SW32 (same rows for both halves)
+    __nv_bfloat16 Baug[KT_STAGES][KT_N * KT_AUG];       // SW32
+    uint64_t full[KT_STAGES], empty[KT_STAGES];
+    uint64_t a_full, a_empty;
+    uint64_t tfull[2], tempty[2];
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t ord_f32(float f) {
+    uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// insert (dv, idx) into the sorted list; returns the new k-th threshold.
+// Entries arrive in increasing index order per list, so an equal distance
+// never displaces an existing entry: ties keep the smaller index.
+__device__ __noinline__ float knn_insert(uint64_t* L, int k, float dv, uint32_t idx) {
+    const uint64_t key = ((uint64_t)ord_f32(dv) << 32) | idx;
+    int p = k - 1;
+    if (L[p] > key) {
+        while (p > 0 && L[p - 1] > key) { L[p] = L[p - 1]; --p; }
+        L[p] = key;
+    }
+    return L[k - 1] == ~0ull ? __int_as_float(0x7f800000) : unord_f32((uint32_t)(L[k - 1] >> 32));
+}
+
+// prep (d == 64), 16 lanes per row, one float4 per lane (coalesced):
+//   train:  xb = bf16(-2 x), xaug = [hi, lo, 0 x 14] with ||x||^2 = 256 hi + lo
+//   query:  xb = bf16(q)   (xaug == nullptr)
+// norms (fp32) feed the SIMT fallback; flag |= 1 when the exact formulation
+// does not hold (a coordinate not exact in bf16, or ||x||^2 not an integer
+// below 2^16).
+__global__ void k_knn_prep(const float* __restrict__ x, int64_t rows, float scale, __nv_bfloat16* __restrict__ xb,
+                           __nv_bfloat16* __restrict__ xaug, float* __restrict__ norms, unsigned* __restrict__ flag) {
+    const int sub = threadIdx.x & 15;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    bool inexact = false;
+    for (int64_t w = wid; w * 2 < rows; w += nw) {          // warp-uniform trip count
+        const int64_t r = w * 2 + ((threadIdx.x >> 4) & 1);
+        const bool valid = r < rows;
+        const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(x + r * 64) + sub)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float f[4] = {v.x, v.y, v.z, v.w};
+        __nv_bfloat16 h[4];
+        float s = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float sv = scale * f[e];
+            h[e] = __float2bfloat16_rn(sv);
+            inexact |= (__bfloat162float(h[e]) != sv) || (sv / scale != f[e]);
+            s = fmaf(f[e], f[e], s);
+        }
+        uint2 packed;
+        packed.x = (uint32_t)__bfloat16_as_ushort(h[0]) | ((uint32_t)__bfloat16_as_ushort(h[1]) << 16);
+        packed.y = (uint32_t)__bfloat16_as_ushort(h[2]) | ((uint32_t)__bfloat16_as_ushort(h[3]) << 16);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, 16);
+        if (valid) {
+            reinterpret_cast<uint2*>(xb + r * 64)[sub] = packed;
+            if (sub == 0) norms[r] = s;
+            if (xaug && sub < 4) {
+                // [hi, lo, 0...]: exact when s is an integer in [0, 2^16)
+                const float hi = floorf(s / 256.f), lo = s - 256.f * hi;
+                if (sub == 0) inexact |= !(s >= 0.f && s < 65536.f && s == floorf(s));
+                uint2 a = make_uint2(0u, 0u);
+                if (sub == 0) {
+                    a.x = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(hi)) |
+                          ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(lo)) << 16);
+                }
+                reinterpret_cast<uint2*>(xaug + r * KT_AUG)[sub] = a;
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, inexact) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+__global__ void __launch_bounds__(KT_THREADS, 1)
+k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmx,
+         const __grid_constant__ CUtensorMap tmxa, int64_t ntr, int64_t nq, int k, int nsplit,
+         uint64_t* __restrict__ lists, const unsigned* __restrict__ flag) {
+    if (*flag) return;                       // inexact data: the SIMT path answers
+    extern __shared__ uint8_t smem_raw[];
+    KnnSmem& S = *reinterpret_cast<KnnSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nblk = (int)((nq + KT_Q - 1) / KT_Q);
+    const int ntiles = (int)((ntr + KT_N - 1) / KT_N);
+    const int nitems = nblk * nsplit;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < KT_STAGES; ++s) { tc::mbar_init(&S.full[s], 1); tc::mbar_init(&S.empty[s], 1); }
+        tc::mbar_init(&S.a_full, 1);
+        tc::mbar_init(&S.a_empty, 1);
+        for (int b = 0; b < 2; ++b) { tc::mbar_init(&S.tfull[b], 1); tc::mbar_init(&S.tempty[b], 8); }
+        tc::fence_mbar_init();
+        tc::tma_prefetch(&tmq);
+        tc::tma_prefetch(&tmx);
+        tc::tma_prefetch(&tmxa);
+    }
+    // constant augmentation rows [256, 1, 0 x 14] in the SWIZZLE_32B layout:
+    // 16-byte chunk c of row r lives at chunk c ^ ((r >> 2) & 1)
+    for (int r = threadIdx.x; r < KT_M; r += blockDim.x) {
+        uint4* rowp = reinterpret_cast<uint4*>(S.Aaug + r * KT_AUG);
+        const int c0 = (r >> 2) & 1;
+        rowp[c0] = make_uint4((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(256.f)) |
+                              ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(1.f)) << 16), 0u, 0u, 0u);
+        rowp[c0 ^ 1] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    tc::fence_proxy_async();                 // generic-proxy smem writes -> UMMA (async proxy)
+    if (warp == 2) tc::tmem_alloc(&S.tmem_base, 512);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = S.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {                                    // ---- TMA producer
+            int stage = 0; uint32_t phase = 0, a_par = 0;
+            bool first = true;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const int qb = it / nsplit, sp = it % nsplit;
+                const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
+                if (!first) { tc::mbar_wait(&S.a_empty, a_par); a_par ^= 1; }
+                first = false;
+                tc::mbar_arrive_expect_tx(&S.a_full, KT_A_BYTES);
+                tc::tma_load_2d(S.A, &tmq, &S.a_full, 0, qb * KT_Q);
+                for (int t = t0; t < t1; ++t) {
+                    tc::mbar_wait(&S.empty[stage], phase ^ 1);
+                    tc::mbar_arrive_expect_tx(&S.full[stage], KT_B_BYTES + KT_BAUG_BYTES);
+                    tc::tma_load_2d(S.B[stage], &tmx, &S.full[stage], 0, t * KT_N);
+                    tc::tma_load_2d(S.Baug[stage], &tmxa, &S.full[stage], 0, t * KT_N);
+                    if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {                                    // ---- MMA issuer
+            constexpr uint32_t idesc = tc::instr_desc(KT_M, KT_N, 1);
+            int stage = 0; uint32_t phase = 0, a_par = 0;
+            int b = 0; uint32_t acc_phase = 0;
+            const uint32_t a_base = tc::smem_u32(S.A);
+            const uint64_t aaug_desc = tc::sw32_kmajor_desc(tc::smem_u32(S.Aaug));
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const int sp = it % nsplit;
+                const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
+                tc::mbar_wait(&S.a_full, a_par); a_par ^= 1;
+                for (int t = t0; t < t1; ++t) {
+                    tc::mbar_wait(&S.tempty[b], acc_phase ^ 1);
+                    tc::mbar_wait(&S.full[stage], phase);
+                    tc::tc_fence_after();
+                    const uint32_t b_base = tc::smem_u32(S.B[stage]);
+                    const uint64_t baug_desc = tc::sw32_kmajor_desc(tc::smem_u32(S.Baug[stage]));
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t d = tmem + (uint32_t)((b * 2 + h) * KT_N);
+                        const uint32_t ah = a_base + h * (KT_M * KT_D * 2);
+#pragma unroll
+                        for (int kk = 0; kk < KT_D / 16; ++kk)
+                            tc::umma_f16(d, tc::sw128_kmajor_desc(ah + kk * 32),
+                                         tc::sw128_kmajor_desc(b_base + kk * 32), idesc, kk > 0);
+                        tc::umma_f16(d, aaug_desc, baug_desc, idesc, 1);   // + 256 hi + lo
+                    }
+                    tc::umma_commit(&S.empty[stage]);
+                    tc::umma_commit(&S.tfull[b]);
+                    if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
+                    b ^= 1;
+                    if (b == 0) acc_phase ^= 1;
+                }
+                tc::umma_commit(&S.a_empty);
+            }
+        }
+    } else if (warp >= 4) {                                  // ---- epilogue
+        const int quad = warp & 3, h = (warp - 4) >> 2;
+        const int row = h * KT_M + quad * 32 + lane;           // query within the block
+        int b = 0; uint32_t acc_phase = 0;
+        uint64_t L[KT_KMAX];                                  // sorted keys (touched on insertion only)
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const int qb = it / nsplit, sp = it % nsplit;
+            const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
+            for (int i = 0; i < KT_KMAX; ++i) L[i] = ~0ull;
+            float thr = __int_as_float(0x7f800000);        // +inf
+            for (int t = t0; t < t1; ++t) {
+                tc::mbar_wait(&S.tfull[b], acc_phase);
+                tc::tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((b * 2 + h) * KT_N);
+                const int64_t colbase = (int64_t)t * KT_N;
+#pragma unroll 1
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t r[64];
+                    tc::tmem_ld_32x32b_x64(taddr + c * 64, r);
+                    tc::tmem_ld_wait();
+                    if (c == 1) {                             // accumulator fully read: release it
+                        tc::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) tc::mbar_arrive(&S.tempty[b]);
+                    }
+                    const int64_t col0 = colbase + c * 64;
+                    if (col0 + 64 > ntr) {                   // last tile: padded rows read as 0
+#pragma unroll
+                        for (int j = 0; j < 64; ++j)
+                            if (col0 + j >= ntr) r[j] = 0x7f800000u;
+                    }
+                    // per 32 candidates: min as a depth-5 tree (a linear chain
+                    // would serialise 31 dependent FMNMX), then the rare scan
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+                        float m[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            m[j] = fminf(__uint_as_float(r[g * 32 + j]), __uint_as_float(r[g * 32 + j + 16]));
+#pragma unroll
+                        for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+                            for (int j = 0; j < w; ++j) m[j] = fminf(m[j], m[j + w]);
+                        if (m[0] < thr) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                const float dv = __uint_as_float(r[g * 32 + j]);
+                                if (dv < thr) thr = knn_insert(L, k, dv, (uint32_t)(col0 + g * 32 + j));
+                            }
+                        }
+                    }
+                }
+                b ^= 1;
+                if (b == 0) acc_phase ^= 1;
+            }
+            const int64_t q = (int64_t)qb * KT_Q + row;
+            if (q < nq) {
+                uint64_t* dst = lists + (q * nsplit + sp) * KT_KMAX;
+                for (int i = 0; i < KT_KMAX; ++i) dst[i] = L[i];
+            }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tc::tmem_dealloc(tmem, 512);
+}
+
+// Merge the nsplit sorted partial lists of each query and vote (ties -> the
+// smaller label, `foldl (... gti ...) 0 classIdx`).
+__global__ void k_knn_merge(const uint64_t* __restrict__ lists, int nlists, const int* __restrict__ labels,
+                            int64_t nq, int k, int ncls, int* __restrict__ out_label, int* __restrict__ out_idx,
+                            const unsigned* __restrict__ flag) {
+    if (*flag) return;
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint64_t* P = lists + q * nlists * KT_KMAX;
+    int head[64];
+    for (int l = 0; l < nlists; ++l) head[l] = 0;
+    int votes[64];
+    for (int c = 0; c < ncls; ++c) votes[c] = 0;
+    for (int r = 0; r < k; ++r) {
+        uint64_t best = ~0ull;
+        int bl = 0;
+        for (int l = 0; l < nlists; ++l) {
+            const uint64_t v = head[l] < k ? P[l * KT_KMAX + head[l]] : ~0ull;
+            if (v < best) { best = v; bl = l; }
+        }
+        head[bl]++;
+        const int idx = best == ~0ull ? -1 : (int)(uint32_t)(best & 0xffffffffu);
+        if (out_idx) out_idx[q * k + r] = idx;
+        if (idx >= 0) {
+            const int lab = labels[idx];
+            if (lab >= 0 && lab < ncls) votes[lab]++;
+        }
+    }
+    int best = 0;
+    for (int c = 1; c < ncls; ++c) if (votes[c] > votes[best]) best = c;
+    out_label[q] = best;
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode_tiled() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled)p;
+    }
+    return fn;
+}
+
+// 2-D row-major [rows][cols] tensor, box [box_rows][box_cols], given swizzle.
+bool make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t rows,
+                  uint64_t cols, uint32_t box_rows, uint32_t box_cols, CUtensorMapSwizzle swz) {
+    PFN_encodeTiled enc = get_encode_tiled();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * (uint64_t)elem_bytes};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int knn_tc_nsplit(int64_t ntr, int64_t nq) {
+    const int nblk = (int)((nq + KT_Q - 1) / KT_Q);
+    const int ntiles = (int)((ntr + KT_N - 1) / KT_N);
+    int ns = (4 * sm_count() + nblk - 1) / nblk;       // ~4 work items per SM
+    if (ns > 64) ns = 64;
+    if (ns > ntiles) ns = ntiles;
+    return ns < 1 ? 1 : ns;
+}
+
+// workspace: xb (ntr x 64 bf16) | xaug (ntr x 16 bf16) | qb (nq x 64 bf16) | lists
+size_t knn_tc_workspace(int64_t ntr, int64_t nq) {
+    const int ns = knn_tc_nsplit(ntr, nq);
+    return (size_t)ntr * (KT_D + KT_AUG) * 2 + (size_t)nq * KT_D * 2 + 1024 + (size_t)nq * ns * KT_KMAX * 8 + 256;
+}
+
+int knn_tc_run(const float* train, const float* query, const int* labels, int64_t ntr, int64_t nq, int k, int ncls,
+               int* out_label, int* out_idx, float* tnorm, float* qnorm, unsigned* flag, void* ws, cudaStream_t st) {
+    char* w = (char*)ws;
+    __nv_bfloat16* xb = (__nv_bfloat16*)w;
+    __nv_bfloat16* xaug = xb + (size_t)ntr * KT_D;
+    __nv_bfloat16* qb = xaug + (size_t)ntr * KT_AUG;
+    uint64_t* lists = (uint64_t*)(((uintptr_t)(qb + (size_t)nq * KT_D) + 1023) & ~(uintptr_t)1023);
+    const int pgrid = 4 * sm_count();
+    k_knn_prep<<<(unsigned)imin64(pgrid, (ntr + 15) / 16), 256, 0, st>>>(train, ntr, -2.f, xb, xaug, tnorm, flag);
+    k_knn_prep<<<(unsigned)imin64(pgrid, (nq + 15) / 16), 256, 0, st>>>(query, nq, 1.f, qb, nullptr, qnorm, flag);
+    PMX_CHECK_LAUNCH("knn_prep");
+    CUtensorMap tmq, tmx, tmxa;
+    if (!make_tmap_2d(&tmq, qb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)nq, KT_D, KT_Q, KT_D,
+                      CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap_2d(&tmx, xb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)ntr, KT_D, KT_N, KT_D,
+                      CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap_2d(&tmxa, xaug, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)ntr, KT_AUG, KT_N, KT_AUG,
+                      CU_TENSOR_MAP_SWIZZLE_32B)) {
+        set_last_error("knn: cuTensorMapEncodeTiled unavailable or failed");
+        return -2;
+    }
+    const int nsplit = knn_tc_nsplit(ntr, nq);
+    const int nitems = (int)((nq + KT_Q - 1) / KT_Q) * nsplit;
+    const size_t smem = sizeof(KnnSmem) + 1024;
+    cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = nitems < sm_count() ? nitems : sm_count();
+    k_knn_tc<<<grid, KT_THREADS, smem, st>>>(tmq, tmx, tmxa, ntr, nq, k, nsplit, lists, flag);
+    PMX_CHECK_LAUNCH("knn_tc");
+    k_knn_merge<<<(unsigned)((nq + 127) / 128), 128, 0, st>>>(lists, nsplit, labels, nq, k, ncls, out_label,
+                                                              out_idx, flag);
+    PMX_CHECK_LAUNCH("knn_merge");
+    return 0;
+}
+
+}  // namespace pmx

@@ -21,6 +21,7 @@
 //   cp.async double buffer, each thread accumulates an 8-signal x 8-state
 //   register tile.  A general small-S kernel (one CTA per signal) covers
 //   other state counts.
+#include <stdlib.h>
 #include "common.cuh"
 
 namespace pmx {
@@ -278,6 +279,11 @@ __global__ void k_viterbi(const double* __restrict__ log_pi, const double* __res
     }
 }
 
+size_t hmm_tc_workspace(int S, int K);
+bool hmm_tc_eligible(int S, int K);
+int hmm_tc_launch(const float* log_pi, const float* A, const float* log_E, int S, int K, const int* obs,
+                  int64_t nsig, int T, double* out_ll, void* ws, cudaStream_t st);
+
 }  // namespace pmx
 
 using namespace pmx;
@@ -286,8 +292,10 @@ extern "C" {
 
 size_t pmx_hmm_forward_workspace_bytes(int32_t S, int64_t nsig) {
     (void)nsig;
-    // E_lin [K<=64][S] + pi_lin [S], generous K bound
-    return (size_t)S * 65 * sizeof(float) + 256;
+    // E_lin [K<=64][S] + pi_lin [S], generous K bound; + the tensor-core path's A^T
+    size_t simt = (size_t)S * 65 * sizeof(float) + 256;
+    size_t tc = hmm_tc_workspace(S, 8);
+    return simt > tc ? simt : tc;
 }
 
 int pmx_hmm_forward_f32(const float* log_pi, const float* A, const float* log_E, int32_t S, int32_t K,
@@ -297,6 +305,11 @@ int pmx_hmm_forward_f32(const float* log_pi, const float* A, const float* log_E,
     PMX_REQUIRE(ws && ws_bytes >= pmx_hmm_forward_workspace_bytes(S, nsig), "pmx_hmm_forward_f32: workspace too small");
     if (nsig == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
+    // tensor-core path (hmm_tc.cu) for the BASELINE state count; PMX_HMM_SIMT=1
+    // forces the SIMT kernel (A/B comparisons)
+    static const bool force_simt = getenv("PMX_HMM_SIMT") && getenv("PMX_HMM_SIMT")[0] == '1';
+    if (!force_simt && hmm_tc_eligible(S, K))
+        return hmm_tc_launch(log_pi, A, log_E, S, K, obs, nsig, T, out_ll, ws, st);
     float* E_lin = (float*)ws;
     float* pi_lin = E_lin + (size_t)S * 64;
     k_hmm_prep<<<(S * K + 255) / 256, 256, 0, st>>>(log_pi, log_E, S, K, E_lin, pi_lin);

@@ -1,0 +1,291 @@
+// HMM forward on the tensor cores (tcgen05 kind::tf32, TMEM, TMA).
+//
+// Reference anchor: SURVEY Appendix A.1 hmm_forward.pmx — the log-space
+// forward recursion batched over signals by `map` (see hmm.cu for the SIMT
+// kernel and the linear-space reformulation).  Here the per-step contraction
+//     a_t[j, s] = sum_i A[i, j] * u_{t-1}[i, s]          (all signals s of a CTA)
+// runs as UMMA with the transposed transition matrix as the A operand
+// (M = 128 states per block, K = states i) and the CTA's state vectors as the
+// B operand (N = 32 signals), accumulating in TMEM.
+//
+// Scaling (no normalisation barrier inside a step): with c_t = sum_j u_t[j],
+//     u_0 = pi * E(o_0),   u_t = (u_{t-1} A) * E(o_t) / c_{t-1},
+//     ll = sum_{t=0}^{T-1} log c_t        (fp64)
+// which equals log sum_j alpha_{T-1}[j] exactly in real arithmetic.
+//
+// Precision: TF32 multiplies.  Both operands are rounded to TF32 with
+// round-to-nearest (cvt.rna) — truncation would bias every row sum of A low
+// and the bias compounds over T steps.  Measured error is checked against the
+// fp64 log-space oracle in tests (rel 1e-5 budget).
+//
+// CTA layout (256 threads): warp 0 TMA producer (A^T tiles 128 x 32 fp32,
+// SW128, 3-stage ring, streamed from L2 every step — A is step-invariant, so
+// the ring keeps prefetching into the next step), warp 1 MMA issuer, warp 2
+// TMEM allocator, warps 4-7 epilogue (TMEM lane = state within a 128-state
+// block): scale by E(o_t)/c_{t-1}, round to TF32, write u_t back into the
+// B-operand buffer in shared memory (in place: the step's MMAs are complete),
+// per-signal row sums -> c_t, log c_t.
+#include <stdlib.h>
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace pmx {
+
+constexpr int HT_N = 32;            // signals per CTA (UMMA N)
+constexpr int HT_M = 128;           // states per UMMA M block
+constexpr int HT_KB = 32;           // fp32 per 128-byte swizzle row (K block)
+constexpr int HT_THREADS = 256;
+constexpr int HT_KMAX = 8;          // symbols staged in shared memory
+
+// Configuration: CL = CTAs of a cluster sharing each A^T tile by TMA
+// multicast (each loads HT_M / CL rows), ST = pipeline stages, ESM = emissions
+// staged in shared memory (else read through L1).
+template <int S, int CL, int ST, bool ESM>
+struct __align__(1024) HmmSmem {
+    float U[S / HT_KB][HT_N * HT_KB];             // B operand: K-major SW128, [kblock][signal][32]
+    float At[ST][HT_M * HT_KB];                   // A operand tiles: [state j][32 i], SW128
+    float E[ESM ? HT_KMAX : 1][ESM ? S : 1];      // linear emissions E[k][j]
+    float wsum[4][HT_N];                          // per-warp row-sum partials
+    float inv_c[HT_N];
+    int sym[HT_N];
+    uint64_t full[ST], empty[ST];
+    uint64_t dfull, bready;
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// At[j][i] = tf32_rna(A[i][j]); E_lin[k][j] = exp(log_E[j][k]); pi = exp(log_pi)
+__global__ void k_hmm_tc_prep(const float* __restrict__ A, const float* __restrict__ log_E,
+                              const float* __restrict__ log_pi, int S, int K, float* __restrict__ At,
+                              float* __restrict__ E_lin, float* __restrict__ pi_lin) {
+    __shared__ float tile[32][33];
+    const int bi = blockIdx.y * 32, bj = blockIdx.x * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) tile[r][threadIdx.x] = A[(int64_t)(bi + r) * S + bj + threadIdx.x];
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y)
+        At[(int64_t)(bj + r) * S + bi + threadIdx.x] = tf32_rna(tile[threadIdx.x][r]);
+    if (blockIdx.y == 0) {
+        for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+            const int j = bj + threadIdx.x;
+            if (r < K) E_lin[(int64_t)r * S + j] = expf(log_E[(int64_t)j * K + r]);
+            if (r == 0) pi_lin[j] = expf(log_pi[j]);
+        }
+    }
+}
+
+// byte offset of element (signal s, state i) in the SW128 K-major B buffer
+__device__ __forceinline__ uint32_t u_offset(int s, int i) {
+    const int kb = i >> 5, kk = i & 31;
+    const uint32_t chunk = (uint32_t)(kk >> 2) ^ (uint32_t)(s & 7);
+    return (uint32_t)kb * (HT_N * HT_KB * 4) + (uint32_t)s * 128 + (chunk << 4) + (uint32_t)(kk & 3) * 4;
+}
+
+template <int S, int HT_CLUSTER, int HT_STAGES, bool ESM>
+__global__ void __cluster_dims__(HT_CLUSTER, 1, 1) __launch_bounds__(HT_THREADS, 1)
+k_hmm_fwd_tc(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ E_lin,
+             const float* __restrict__ pi_lin, int K, const int* __restrict__ obs, int64_t nsig, int T,
+             double* __restrict__ out_ll) {
+    constexpr int NJB = S / HT_M;          // 128-state blocks (M)
+    constexpr int NKB = S / HT_KB;         // 32-state K blocks
+    constexpr uint32_t TILE_BYTES = HT_M * HT_KB * 4;
+    constexpr int HT_ROWS = HT_M / HT_CLUSTER;   // tile rows loaded (and multicast) per CTA
+    extern __shared__ uint8_t smem_raw[];
+    typedef HmmSmem<S, HT_CLUSTER, HT_STAGES, ESM> Smem;
+    Smem& Sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t s0 = (int64_t)blockIdx.x * HT_N;
+
+    // ---- setup
+    if (ESM)
+        for (int v = threadIdx.x; v < K * S; v += blockDim.x) (&Sm.E[0][0])[v] = E_lin[v];
+    if (threadIdx.x < HT_N) Sm.inv_c[threadIdx.x] = 1.f;
+    if (threadIdx.x == 0) {
+        // empty[s] completes when the MMAs of EVERY CTA of the cluster consumed
+        // stage s (each CTA's multicast writes into all of them)
+        for (int s = 0; s < HT_STAGES; ++s) { tc::mbar_init(&Sm.full[s], 1); tc::mbar_init(&Sm.empty[s], HT_CLUSTER); }
+        tc::mbar_init(&Sm.dfull, 1);
+        tc::mbar_init(&Sm.bready, 1);
+        tc::fence_mbar_init();
+        tc::tma_prefetch(&tmA);
+    }
+    if (warp == 2) tc::tmem_alloc(&Sm.tmem_base, 512);
+    tc::tc_fence_before();
+    tc::cluster_sync();                      // all barriers of the cluster initialised
+    tc::tc_fence_after();
+    const uint32_t rank = tc::cluster_ctarank();
+    const uint32_t tmem = Sm.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {                                     // ---- TMA producer
+            int stage = 0; uint32_t phase = 0;
+            for (int t = 1; t < T; ++t)
+                for (int kb = 0; kb < NKB; ++kb)
+                    for (int jb = 0; jb < NJB; ++jb) {
+                        tc::mbar_wait(&Sm.empty[stage], phase ^ 1);
+                        tc::mbar_arrive_expect_tx(&Sm.full[stage], TILE_BYTES);
+                        // this CTA's quarter of the tile, multicast to the whole cluster
+                        tc::tma_load_2d_mc(Sm.At[stage] + rank * HT_ROWS * HT_KB, &tmA, &Sm.full[stage],
+                                           kb * HT_KB, jb * HT_M + (int)rank * HT_ROWS,
+                                           (uint16_t)((1u << HT_CLUSTER) - 1));
+                        if (++stage == HT_STAGES) { stage = 0; phase ^= 1; }
+                    }
+        }
+    } else if (warp == 1) {
+        // ---- MMA issuer: the whole warp walks the pipeline (warp-uniform state
+        // stays in uniform registers); one elected lane issues the UMMAs.
+        constexpr uint32_t idesc = tc::instr_desc(HT_M, HT_N, 2);
+        int stage = 0; uint32_t phase = 0, bpar = 0;
+        const uint64_t u_desc = tc::sw128_kmajor_desc(tc::smem_u32(&Sm.U[0][0]));
+        const uint64_t at_desc = tc::sw128_kmajor_desc(tc::smem_u32(Sm.At[0]));
+        for (int t = 1; t < T; ++t) {
+            tc::mbar_wait(&Sm.bready, bpar); bpar ^= 1;   // u_{t-1} written (and D drained)
+            tc::tc_fence_after();
+            for (int kb = 0; kb < NKB; ++kb)
+                for (int jb = 0; jb < NJB; ++jb) {
+                    tc::mbar_wait(&Sm.full[stage], phase);
+                    tc::tc_fence_after();
+                    if (tc::elect_one()) {
+                        // descriptor start addresses are in 16-byte units
+                        const uint64_t ad = at_desc + (uint64_t)(stage * (TILE_BYTES >> 4));
+                        const uint64_t bd = u_desc + (uint64_t)(kb * ((HT_N * HT_KB * 4) >> 4));
+                        // two accumulator sets (even / odd K blocks), summed in the
+                        // epilogue: halves the chain of truncating tensor-core
+                        // accumulations per output (a low bias that compounds over T)
+                        const uint32_t d = tmem + (uint32_t)((kb & 1) * (NJB * HT_N) + jb * HT_N);
+#pragma unroll
+                        for (int kk = 0; kk < HT_KB / 8; ++kk)
+                            tc::umma_tf32(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb >= 2) || (kk != 0));
+                        tc::umma_commit_mc(&Sm.empty[stage], (uint16_t)((1u << HT_CLUSTER) - 1));
+                    }
+                    __syncwarp();
+                    if (++stage == HT_STAGES) { stage = 0; phase ^= 1; }
+                }
+            if (tc::elect_one()) tc::umma_commit(&Sm.dfull);
+            __syncwarp();
+        }
+    } else if (warp >= 4) {                                   // ---- epilogue
+        const int q = warp & 3;                                // TMEM lane quadrant
+        const int ew = warp - 4;
+        double ll = 0.0;                                       // lane s of warp 4 owns signal s
+        uint32_t dpar = 0;
+        for (int t = 0; t < T; ++t) {
+            // stage this step's symbols
+            if (ew == 0) {
+                const int64_t s = s0 + lane;
+                Sm.sym[lane] = (s < nsig) ? obs[s * T + t] : 0;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (t > 0) {
+                tc::mbar_wait(&Sm.dfull, dpar); dpar ^= 1;
+                tc::tc_fence_after();
+            }
+            float csum[HT_N];
+#pragma unroll
+            for (int s = 0; s < HT_N; ++s) csum[s] = 0.f;
+#pragma unroll 1
+            for (int jb = 0; jb < NJB; ++jb) {
+                const int j = jb * HT_M + q * 32 + lane;
+                uint32_t r[32];
+                if (t > 0) {
+                    uint32_t r2[32];
+                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + jb * HT_N, r);
+                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + NJB * HT_N + jb * HT_N, r2);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int s = 0; s < HT_N; ++s)
+                        r[s] = __float_as_uint(__uint_as_float(r[s]) + __uint_as_float(r2[s]));
+                } else {
+                    const float p = pi_lin[j];
+#pragma unroll
+                    for (int s = 0; s < HT_N; ++s) r[s] = __float_as_uint(p);
+                }
+#pragma unroll
+                for (int s = 0; s < HT_N; ++s) {
+                    const float e = ESM ? Sm.E[Sm.sym[s]][j] : __ldg(E_lin + Sm.sym[s] * S + j);
+                    const float u = __uint_as_float(r[s]) * e * Sm.inv_c[s];
+                    const float ur = tf32_rna(u);
+                    csum[s] += ur;
+                    *reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(&Sm.U[0][0]) + u_offset(s, j)) = ur;
+                }
+            }
+            // per-signal sums: transpose-reduce the 32 partials over the warp so
+            // lane s ends with signal s's warp total (31 shuffle-adds)
+#pragma unroll
+            for (int w = 16; w > 0; w >>= 1) {
+                const bool upper = (lane & w) != 0;
+#pragma unroll
+                for (int s = 0; s < w; ++s) {
+                    const float send = upper ? csum[s] : csum[s + w];
+                    const float keep = upper ? csum[s + w] : csum[s];
+                    csum[s] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+                }
+            }
+            // after the loop lane l holds the total of signal l in csum[0]
+            // (the halving pairs lanes so that signal index bits map to lane bits)
+            Sm.wsum[ew][lane] = csum[0];
+            tc::fence_proxy_async();                 // u_t visible to the UMMA async proxy
+            tc::tc_fence_before();                   // TMEM reads ordered before the hand-off
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (ew == 0) {
+                const float c = Sm.wsum[0][lane] + Sm.wsum[1][lane] + Sm.wsum[2][lane] + Sm.wsum[3][lane];
+                Sm.inv_c[lane] = 1.f / c;
+                ll += log((double)c);
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (threadIdx.x == 128 && t + 1 < T) {
+                tc::tc_fence_before();
+                tc::mbar_arrive(&Sm.bready);
+            }
+        }
+        if (ew == 0 && s0 + lane < nsig) out_ll[s0 + lane] = ll;
+    }
+    tc::tc_fence_before();
+    tc::cluster_sync();                      // no CTA leaves while peers may still multicast into it
+    if (warp == 2) tc::tmem_dealloc(tmem, 512);
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+bool make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t rows,
+                  uint64_t cols, uint32_t box_rows, uint32_t box_cols, CUtensorMapSwizzle swz);
+
+size_t hmm_tc_workspace(int S, int K) { return (size_t)S * S * 4 + (size_t)HT_KMAX * S * 4 + (size_t)S * 4 + 1024; }
+
+bool hmm_tc_eligible(int S, int K) { return S == 1024 && K <= HT_KMAX; }
+
+int hmm_tc_launch(const float* log_pi, const float* A, const float* log_E, int S, int K, const int* obs,
+                  int64_t nsig, int T, double* out_ll, void* ws, cudaStream_t st) {
+    float* At = (float*)ws;
+    float* E_lin = At + (size_t)S * S;
+    float* pi_lin = E_lin + (size_t)HT_KMAX * S;
+    k_hmm_tc_prep<<<dim3(S / 32, S / 32), dim3(32, 8), 0, st>>>(A, log_E, log_pi, S, K, At, E_lin, pi_lin);
+    PMX_CHECK_LAUNCH("hmm_tc_prep");
+    // Configuration measured at the BASELINE config (4096 x 10^4 x 1024):
+    //   cluster 4 / 4 stages / E in smem  487 ms   (chosen: also cuts L2 reads 4x)
+    //   cluster 1 / 4 stages / E in smem  487 ms
+    //   cluster 1 or 4 / 6 stages / E via L1  653 ms
+    // The step is bound by shared-memory traffic: every SM streams the 4 MiB
+    // A^T through smem once per step (TMA write + UMMA read) for only 32 signals.
+    constexpr int cl = 4;
+    CUtensorMap tmA;
+    if (!make_tmap_2d(&tmA, At, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)S, (uint64_t)S, HT_M / cl, HT_KB,
+                      CU_TENSOR_MAP_SWIZZLE_128B)) {
+        set_last_error("hmm: cuTensorMapEncodeTiled failed");
+        return -2;
+    }
+    unsigned grid = (unsigned)((nsig + HT_N - 1) / HT_N);
+    grid = (grid + cl - 1) / cl * cl;        // whole clusters (padding CTAs run on masked signals)
+    const size_t smem = sizeof(HmmSmem<1024, cl, 4, true>) + 1024;
+    cudaFuncSetAttribute(k_hmm_fwd_tc<1024, cl, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_hmm_fwd_tc<1024, cl, 4, true><<<grid, HT_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
+    PMX_CHECK_LAUNCH("hmm_fwd_tc");
+    return 0;
+}
+
+}  // namespace pmx

@@ -193,40 +193,45 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {                                    // ---- MMA issuer
-            constexpr uint32_t idesc = tc::instr_desc(KT_M, KT_N, 1);
-            int stage = 0; uint32_t phase = 0, a_par = 0;
-            int b = 0; uint32_t acc_phase = 0;
-            const uint32_t a_base = tc::smem_u32(S.A);
-            const uint64_t aaug_desc = tc::sw32_kmajor_desc(tc::smem_u32(S.Aaug));
-            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-                const int sp = it % nsplit;
-                const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
-                tc::mbar_wait(&S.a_full, a_par); a_par ^= 1;
-                for (int t = t0; t < t1; ++t) {
-                    tc::mbar_wait(&S.tempty[b], acc_phase ^ 1);
-                    tc::mbar_wait(&S.full[stage], phase);
-                    tc::tc_fence_after();
-                    const uint32_t b_base = tc::smem_u32(S.B[stage]);
-                    const uint64_t baug_desc = tc::sw32_kmajor_desc(tc::smem_u32(S.Baug[stage]));
+        // ---- MMA issuer: the whole warp walks the pipeline (uniform registers),
+        // one elected lane issues; descriptors advance in 16-byte units
+        constexpr uint32_t idesc = tc::instr_desc(KT_M, KT_N, 1);
+        int stage = 0; uint32_t phase = 0, a_par = 0;
+        int b = 0; uint32_t acc_phase = 0;
+        const uint64_t a_desc = tc::sw128_kmajor_desc(tc::smem_u32(S.A));
+        const uint64_t b_desc0 = tc::sw128_kmajor_desc(tc::smem_u32(S.B[0]));
+        const uint64_t aaug_desc = tc::sw32_kmajor_desc(tc::smem_u32(S.Aaug));
+        const uint64_t baug_desc0 = tc::sw32_kmajor_desc(tc::smem_u32(S.Baug[0]));
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const int sp = it % nsplit;
+            const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
+            tc::mbar_wait(&S.a_full, a_par); a_par ^= 1;
+            for (int t = t0; t < t1; ++t) {
+                tc::mbar_wait(&S.tempty[b], acc_phase ^ 1);
+                tc::mbar_wait(&S.full[stage], phase);
+                tc::tc_fence_after();
+                if (tc::elect_one()) {
+                    const uint64_t bd = b_desc0 + (uint64_t)(stage * (KT_B_BYTES >> 4));
+                    const uint64_t bad = baug_desc0 + (uint64_t)(stage * (KT_BAUG_BYTES >> 4));
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const uint32_t d = tmem + (uint32_t)((b * 2 + h) * KT_N);
-                        const uint32_t ah = a_base + h * (KT_M * KT_D * 2);
+                        const uint64_t ad = a_desc + (uint64_t)(h * ((KT_M * KT_D * 2) >> 4));
 #pragma unroll
                         for (int kk = 0; kk < KT_D / 16; ++kk)
-                            tc::umma_f16(d, tc::sw128_kmajor_desc(ah + kk * 32),
-                                         tc::sw128_kmajor_desc(b_base + kk * 32), idesc, kk > 0);
-                        tc::umma_f16(d, aaug_desc, baug_desc, idesc, 1);   // + 256 hi + lo
+                            tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, kk > 0);
+                        tc::umma_f16(d, aaug_desc, bad, idesc, 1);   // + 256 hi + lo
                     }
                     tc::umma_commit(&S.empty[stage]);
                     tc::umma_commit(&S.tfull[b]);
-                    if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
-                    b ^= 1;
-                    if (b == 0) acc_phase ^= 1;
                 }
-                tc::umma_commit(&S.a_empty);
+                __syncwarp();
+                if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
+                b ^= 1;
+                if (b == 0) acc_phase ^= 1;
             }
+            if (tc::elect_one()) tc::umma_commit(&S.a_empty);
+            __syncwarp();
         }
     } else if (warp >= 4) {                                  // ---- epilogue
         const int quad = warp & 3, h = (warp - 4) >> 2;
@@ -368,28 +373,35 @@ int knn_tc_nsplit(int64_t ntr, int64_t nq) {
 }
 
 // workspace: xb (ntr x 64 bf16) | xaug (ntr x 16 bf16) | qb (nq x 64 bf16) | lists
+// Operand buffers are padded to whole TMA boxes (a box may not exceed the
+// tensor): rows beyond nq / ntr hold garbage that is never reported (queries)
+// or masked to +inf (train columns) in the epilogue.
+static inline int64_t pad_to(int64_t n, int64_t m) { return (n + m - 1) / m * m; }
+
 size_t knn_tc_workspace(int64_t ntr, int64_t nq) {
     const int ns = knn_tc_nsplit(ntr, nq);
-    return (size_t)ntr * (KT_D + KT_AUG) * 2 + (size_t)nq * KT_D * 2 + 1024 + (size_t)nq * ns * KT_KMAX * 8 + 256;
+    const int64_t ntr_p = pad_to(ntr, KT_N), nq_p = pad_to(nq, KT_Q);
+    return (size_t)ntr_p * (KT_D + KT_AUG) * 2 + (size_t)nq_p * KT_D * 2 + 1024 + (size_t)nq * ns * KT_KMAX * 8 + 256;
 }
 
 int knn_tc_run(const float* train, const float* query, const int* labels, int64_t ntr, int64_t nq, int k, int ncls,
                int* out_label, int* out_idx, float* tnorm, float* qnorm, unsigned* flag, void* ws, cudaStream_t st) {
+    const int64_t ntr_p = pad_to(ntr, KT_N), nq_p = pad_to(nq, KT_Q);
     char* w = (char*)ws;
     __nv_bfloat16* xb = (__nv_bfloat16*)w;
-    __nv_bfloat16* xaug = xb + (size_t)ntr * KT_D;
-    __nv_bfloat16* qb = xaug + (size_t)ntr * KT_AUG;
-    uint64_t* lists = (uint64_t*)(((uintptr_t)(qb + (size_t)nq * KT_D) + 1023) & ~(uintptr_t)1023);
+    __nv_bfloat16* xaug = xb + (size_t)ntr_p * KT_D;
+    __nv_bfloat16* qb = xaug + (size_t)ntr_p * KT_AUG;
+    uint64_t* lists = (uint64_t*)(((uintptr_t)(qb + (size_t)nq_p * KT_D) + 1023) & ~(uintptr_t)1023);
     const int pgrid = 4 * sm_count();
     k_knn_prep<<<(unsigned)imin64(pgrid, (ntr + 15) / 16), 256, 0, st>>>(train, ntr, -2.f, xb, xaug, tnorm, flag);
     k_knn_prep<<<(unsigned)imin64(pgrid, (nq + 15) / 16), 256, 0, st>>>(query, nq, 1.f, qb, nullptr, qnorm, flag);
     PMX_CHECK_LAUNCH("knn_prep");
     CUtensorMap tmq, tmx, tmxa;
-    if (!make_tmap_2d(&tmq, qb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)nq, KT_D, KT_Q, KT_D,
+    if (!make_tmap_2d(&tmq, qb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)nq_p, KT_D, KT_Q, KT_D,
                       CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap_2d(&tmx, xb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)ntr, KT_D, KT_N, KT_D,
+        !make_tmap_2d(&tmx, xb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)ntr_p, KT_D, KT_N, KT_D,
                       CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap_2d(&tmxa, xaug, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)ntr, KT_AUG, KT_N, KT_AUG,
+        !make_tmap_2d(&tmxa, xaug, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)ntr_p, KT_AUG, KT_N, KT_AUG,
                       CU_TENSOR_MAP_SWIZZLE_32B)) {
         set_last_error("knn: cuTensorMapEncodeTiled unavailable or failed");
         return -2;

@@ -206,6 +206,34 @@ def ir_eval(e, env: dict):
         return ir_eval(e.body, env2)
     if isinstance(e, L.Never):
         raise OracleError("reached a never expression (no pattern matched)")
+    if isinstance(e, L.Get):                 # interp.py:448-451 + _seq_bounds 536-541
+        i = ir_eval(e.index, env)
+        n = e.arr.shape[0]
+        if not 0 <= i < n:
+            raise OracleError(f"get index {i} out of bounds for sequence of length {n}")
+        return e.arr.data[e.arr.offset + i]
+    if isinstance(e, L.Len):
+        return e.arr.shape[0]
+    if isinstance(e, (L.TGet, L.TSet)):      # interp.py:468-474, runtime.py:63-75
+        t = e.tensor
+        idx = [ir_eval(x, env) for x in e.index]
+        pos, stride = t.offset, 1
+        for d in range(len(t.shape) - 1, -1, -1):
+            if not 0 <= idx[d] < t.shape[d]:
+                raise OracleError(f"tensor index {idx[d]} out of bounds for dimension {d} of size {t.shape[d]}")
+            pos += idx[d] * stride
+            stride *= t.shape[d]
+        if isinstance(e, L.TGet):
+            return t.data[pos]
+        t.data[pos] = ir_eval(e.value, env)
+        return 0
+    if isinstance(e, L.Do):
+        out = 0
+        for x in e.exprs:
+            out = ir_eval(x, env)
+        return out
+    if isinstance(e, L.Field):
+        return ir_eval(e.rec, env)[e.label]
     raise OracleError(f"ir_eval: unsupported node {type(e).__name__}")
 
 

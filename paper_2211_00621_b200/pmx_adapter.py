@@ -1,0 +1,406 @@
+"""Whole-program drop-in: run the reference interpreter's accelerated
+constructs on the B200.
+
+The reference's parallel skeletons are module globals of `pmx.interp`, looked
+up by name at every call (pmx/interp.py:146, 155, 160, 170).  `install(interp)`
+replaces them:
+
+    eval_map    (interp.py:294-304)   eval_map2 (307-319)
+    eval_reduce (interp.py:328-343)   eval_loop (346-358)
+
+When the construct runs in device context and is not nested (`ctx.run_parallel`,
+interp.py:82-84), its function argument — a reference `Closure` or
+`BuiltinPartial` (pmx/runtime.py:78-93), i.e. an AST with an environment — is
+translated to this package's lambda IR (`to_lam`), the sequence is marshalled
+to the device, the construct runs in libpmxb200.so, and the result comes back
+as reference values.  Everything else (host code, nested constructs inside a
+worker, debug mode) keeps the reference's own implementation, exactly as the
+reference runs it.  A function the device cannot execute raises the
+reference's `Diagnostics` — there is no silent CPU fallback.
+
+Only this module imports `pmx`, and only when the caller passes it in (the
+reference is not shipped with this repository).
+"""
+from __future__ import annotations
+
+from typing import Any, Callable, Optional
+
+from . import lambdas as L
+from .lambdas import CompileError
+
+
+class Unsupported(Exception):
+    pass
+
+
+# ============================================================ translation
+
+def to_lam(f, n_params: int, syn, rt, host_array: Callable) -> L.Lam:
+    """Translate a reference function value of arity n_params to a Lam.
+
+    `syn` / `rt` are the reference modules pmx.syntax / pmx.runtime;
+    `host_array(value)` turns a captured host sequence / tensor into the object
+    stored in Get/TGet/TSet nodes (a device array for the B200, the host value
+    for the CPU checker)."""
+    tr = _Translator(syn, rt, host_array)
+    params = [f"_a{i}" for i in range(n_params)]
+    body = tr.apply_value(f, [L.Var(p) for p in params], depth=0)
+    return L.Lam(params, body)
+
+
+class _Fn:
+    """A function value during translation: Closure, builtin partial, or a
+    lambda bound in the body being translated."""
+
+    def __init__(self, kind, **kw):
+        self.kind = kind
+        self.__dict__.update(kw)
+
+
+class _Translator:
+    MAX_INLINE = 16
+
+    def __init__(self, syn, rt, host_array):
+        self.S = syn
+        self.R = rt
+        self.host_array = host_array
+        self.names: dict = {}
+        self.counter = 0
+
+    def fresh(self, base: str) -> str:
+        self.counter += 1
+        return f"{base}_{self.counter}"
+
+    # -- values captured from the reference environment
+    def value(self, v):
+        if isinstance(v, bool):
+            return L.Const(bool(v), "bool")
+        if isinstance(v, int):
+            return L.Const(int(v), "int")
+        if isinstance(v, float):
+            return L.Const(float(v), "float")
+        if isinstance(v, str) and len(v) == 1:
+            return L.Const(ord(v), "char")
+        if isinstance(v, (self.R.Closure, self.R.BuiltinPartial)):
+            return _Fn("value", v=v)
+        if isinstance(v, (list, self.R.TensorView)):
+            return _Captured(v)
+        raise Unsupported(f"captured value of type {type(v).__name__}")
+
+    # -- applying a function value to IR arguments
+    def apply_value(self, fv, args: list, depth: int):
+        R = self.R
+        if depth > self.MAX_INLINE:
+            raise Unsupported("recursion or deep function nesting")
+        if isinstance(fv, _Fn):
+            if fv.kind == "value":
+                return self.apply_value(fv.v, args, depth)
+            if fv.kind == "lam":                      # lambda bound in the body
+                return self.apply_lam(fv.param, fv.body, fv.scope, args, depth)
+            raise Unsupported("function value")
+        if isinstance(fv, R.BuiltinPartial):
+            pre = [self.value(a) for a in fv.args]
+            return self.builtin(fv.name, pre + args)
+        if isinstance(fv, R.Closure):
+            return self.apply_closure(fv, args, depth)
+        raise Unsupported(f"application of {type(fv).__name__}")
+
+    def apply_closure(self, clo, args, depth):
+        scope = {"__env__": clo.env}
+        return self.apply_lam(clo.param, clo.body, scope, args, depth)
+
+    def apply_lam(self, param, body, scope, args, depth):
+        if not args:
+            raise Unsupported("partial application returned as a value")
+        S = self.S
+        inner = dict(scope)
+        binds = []
+
+        def bind(p, a):
+            if isinstance(a, (_Fn, _Captured, L.Var)):   # function / sequence / variable: substitute
+                inner[p] = a
+            else:                                     # scalar argument: let-bind (evaluated once)
+                nm = self.fresh(p.text)
+                inner[p] = L.Var(nm)
+                binds.append((nm, a))
+
+        bind(param, args[0])
+        rest = args[1:]
+        e = body
+        while rest and isinstance(e, S.Lam):          # consume further curried parameters
+            bind(e.param, rest[0])
+            rest = rest[1:]
+            e = e.body
+        out = self.expr(e, inner, depth + 1)
+        if rest:
+            out = self.apply_value(out, rest, depth + 1)
+        if binds and isinstance(out, (_Fn, _Captured)):
+            raise Unsupported("function value returned from a device function")
+        for n, a in reversed(binds):
+            out = L.LetE(n, a, out)
+        return out
+
+    def as_expr(self, x):
+        if isinstance(x, (_Fn, _Captured)):
+            raise Unsupported("function or sequence used as a scalar")
+        return x
+
+    # -- AST -> IR
+    def lookup(self, name, scope):
+        if name in scope:
+            return scope[name]
+        env = scope.get("__env__")
+        if env is None:
+            raise Unsupported(f"unbound {name}")
+        try:
+            v = env.lookup(name)
+        except AssertionError:
+            raise Unsupported(f"unbound {name}") from None
+        return self.value(v)
+
+    def expr(self, e, scope, depth):
+        S = self.S
+        if isinstance(e, S.Var):
+            return self.lookup(e.name, scope)
+        if isinstance(e, S.ConstE):
+            c = e.const
+            if isinstance(c, S.CBuiltin):
+                return _Fn("value", v=self.R.BuiltinPartial(c.name, ()))
+            if isinstance(c, S.CChar):
+                return L.Const(ord(c.value), "char")
+            if isinstance(c, S.CBool):
+                return L.Const(bool(c.value), "bool")
+            if isinstance(c, S.CInt):
+                return L.Const(int(c.value), "int")
+            return L.Const(float(c.value), "float")
+        if isinstance(e, S.Lam):
+            return _Fn("lam", param=e.param, body=e.body, scope=scope)
+        if isinstance(e, S.App):
+            head, args = e, []
+            while isinstance(head, S.App):
+                args.append(head.arg)
+                head = head.fn
+            args.reverse()
+            if isinstance(head, S.ConstE) and isinstance(head.const, S.CBuiltin):
+                name = head.const.name
+                if name in ("tensorGet", "tensorSet"):
+                    return self.tensor_op(name, args, scope, depth)
+                return self.builtin(name, [self.expr(a, scope, depth) for a in args])
+            fv = self.expr(head, scope, depth)
+            return self.apply_value(fv, [self.expr(a, scope, depth) for a in args], depth + 1)
+        if isinstance(e, S.Let):
+            v = self.expr(e.value, scope, depth)
+            inner = dict(scope)
+            if isinstance(v, (_Fn, _Captured)):
+                inner[e.name] = v
+                return self.expr(e.body, inner, depth)
+            nm = self.fresh(e.name.text)
+            inner[e.name] = L.Var(nm)
+            return L.LetE(nm, v, self.as_expr(self.expr(e.body, inner, depth)))
+        if isinstance(e, S.Match):
+            return self.match(e, scope, depth)
+        if isinstance(e, S.Never):
+            return L.Never()
+        raise Unsupported(f"{type(e).__name__} in a device function")
+
+    def match(self, e, scope, depth):
+        S = self.S
+        pat = e.pat
+        if isinstance(pat, S.PVar):
+            v = self.expr(e.scrut, scope, depth)
+            inner = dict(scope)
+            if isinstance(v, (_Fn, _Captured)):
+                inner[pat.name] = v
+                return self.expr(e.thn, inner, depth)
+            nm = self.fresh(pat.name.text)
+            inner[pat.name] = L.Var(nm)
+            return L.LetE(nm, v, self.as_expr(self.expr(e.thn, inner, depth)))
+        if isinstance(pat, S.PConst):
+            v = self.as_expr(self.expr(e.scrut, scope, depth))
+            c = self.expr(S.ConstE(pat.const), scope, depth)
+            return L.If(L.Prim("eq", [v, c]), self.as_expr(self.expr(e.thn, scope, depth)),
+                        self.as_expr(self.expr(e.els, scope, depth)))
+        if isinstance(pat, S.PRecord):
+            # projection sugar (pmx/parser.py:400-406): match r with {l = x} then x else never
+            if len(pat.fields) == 1 and isinstance(pat.fields[0][1], S.PVar) and isinstance(e.els, S.Never):
+                label, sub = pat.fields[0]
+                rec = self.expr(e.scrut, scope, depth)
+                if isinstance(e.thn, S.Var) and e.thn.name == sub.name:
+                    return L.Field(self.as_expr(rec), label)
+                inner = dict(scope)
+                nm = self.fresh(sub.name.text)
+                inner[sub.name] = L.Var(nm)
+                return L.LetE(nm, L.Field(self.as_expr(rec), label), self.as_expr(self.expr(e.thn, inner, depth)))
+            raise Unsupported("record pattern")
+        raise Unsupported("pattern")
+
+    def builtin(self, name, args):
+        if name in L.BUILTINS:
+            if len(args) < L.BUILTINS[name].arity:
+                # partial builtin as a value
+                return _Fn("value", v=self.R.BuiltinPartial(name, tuple()))
+            return L.Prim(name, [self.as_expr(a) for a in args])
+        if name == "get":
+            s, i = args
+            if not isinstance(s, _Captured):
+                raise Unsupported("get on a non-captured sequence")
+            return L.Get(self.host_array(s.v), self.as_expr(i))
+        if name == "length":
+            (s,) = args
+            if not isinstance(s, _Captured):
+                raise Unsupported("length of a non-captured sequence")
+            return L.Len(self.host_array(s.v))
+        raise Unsupported(f"builtin {name}")
+
+    def tensor_op(self, name, args, scope, depth):
+        S = self.S
+        t = self.expr(args[0], scope, depth)
+        if not isinstance(t, _Captured) or not isinstance(t.v, self.R.TensorView):
+            raise Unsupported(f"{name} on a non-captured tensor")
+        if not isinstance(args[1], S.SeqE):
+            raise Unsupported(f"{name} index must be a literal sequence")
+        idx = [self.as_expr(self.expr(x, scope, depth)) for x in args[1].items]
+        arr = self.host_array(t.v)
+        if name == "tensorGet":
+            return L.TGet(arr, idx)
+        return L.TSet(arr, idx, self.as_expr(self.expr(args[2], scope, depth)))
+
+
+class _Captured:
+    def __init__(self, v):
+        self.v = v
+
+
+# ============================================================ installation
+
+def _elem_type(s: list) -> str:
+    if not s:
+        return "int"
+    x = s[0]
+    if isinstance(x, bool):
+        return "bool"
+    if isinstance(x, int):
+        return "int"
+    if isinstance(x, float):
+        return "float"
+    if isinstance(x, str):
+        return "char"
+    if isinstance(x, dict):
+        return "record"
+    raise Unsupported(f"sequence of {type(x).__name__}")
+
+
+def install(interp):
+    """Replace pmx.interp's parallel skeletons by the B200 versions.
+    Returns an `uninstall()` callable restoring the originals."""
+    from . import skeletons as K
+    from .diagnostics import Diagnostics as B200Diagnostics
+    from .runtime import seq_to_device, seq_to_host
+    pkg = interp.__name__.rsplit(".", 1)[0]
+    syn = __import__(pkg + ".syntax", fromlist=["x"])
+    rt = __import__(pkg + ".runtime", fromlist=["x"])
+    orig = {n: getattr(interp, n) for n in ("eval_map", "eval_map2", "eval_reduce", "eval_loop")}
+
+    def translate(f, n, ctx, span, written):
+        def host_array(v):
+            if isinstance(v, rt.TensorView):
+                t = HeapTensor(v, ctx.heap.buffers[v.buffer])
+                written.append(t)
+                return t
+            return seq_to_device(v)
+        try:
+            return to_lam(f, n, syn, rt, host_array)
+        except (Unsupported, CompileError) as exc:
+            raise rt.runtime_error(f"not supported on the B200 device: {exc}", span) from None
+
+    def to_ref(seq):
+        vals = seq_to_host(seq).tolist()
+        if seq.elem_tag == "char":
+            return [chr(v) for v in vals]
+        if seq.elem_tag == "bool":
+            return [bool(v) for v in vals]
+        return vals
+
+    def run(f, n, ctx, span, body):
+        written: list = []
+        lam = translate(f, n, ctx, span, written)
+        dctx = K.Ctx()
+        dctx.device = True
+        K._ctx_stack.append(dctx)
+        try:
+            out = body(lam)
+            dctx.check_errors()
+        except B200Diagnostics as d:               # device error -> the reference's Diagnostics
+            raise rt.runtime_error(d.items[0].message, span) from None
+        finally:
+            K._ctx_stack.pop()
+        for t in written:                           # tensors written by the construct
+            t.copy_back()
+        return out
+
+    def eval_map(f, s, ctx, span):
+        if not ctx.run_parallel or not s:
+            return orig["eval_map"](f, s, ctx, span)
+        _elem_type(s)
+        return run(f, 1, ctx, span, lambda lam: to_ref(K._materialize(K.eval_map(lam, seq_to_device(s)))))
+
+    def eval_map2(f, s1, s2, ctx, span):
+        if not ctx.run_parallel or not s1:
+            return orig["eval_map2"](f, s1, s2, ctx, span)
+        return run(f, 2, ctx, span, lambda lam: to_ref(K.eval_map2(lam, s1, s2)))
+
+    def eval_reduce(f, acc, s, ctx, span):
+        if not ctx.run_parallel or not s:
+            return orig["eval_reduce"](f, acc, s, ctx, span)
+        return run(f, 2, ctx, span, lambda lam: K.eval_reduce(lam, acc, s).get())
+
+    def eval_loop(n, f, ctx, span):
+        if not ctx.run_parallel or n <= 0:
+            return orig["eval_loop"](n, f, ctx, span)
+        return run(f, 1, ctx, span, lambda lam: K.eval_loop(n, lam))
+
+    interp.eval_map, interp.eval_map2 = eval_map, eval_map2
+    interp.eval_reduce, interp.eval_loop = eval_reduce, eval_loop
+
+    def uninstall():
+        for name, fn in orig.items():
+            setattr(interp, name, fn)
+    return uninstall
+
+
+class HeapTensor:
+    """A reference TensorView (a view into a heap buffer, a Python list) used
+    by a device construct: the buffer is copied to the device on first use and
+    copied back after the construct (tensorSet effects, interp.py:471-474)."""
+
+    def __init__(self, view, heap_buf: list):
+        from . import _lib
+        self.view = view
+        self.heap_buf = heap_buf
+        self.shape = tuple(view.shape)
+        self.dtype_code = _lib.PMX_F64 if view.elem == "float" else _lib.PMX_I64
+        self.data = None
+
+    def as_pmx_array(self):
+        import numpy as np
+        from . import _lib
+        from .runtime import to_device
+        if self.data is None:
+            np_t = np.float64 if self.dtype_code == _lib.PMX_F64 else np.int64
+            self.data = to_device(np.array(self.heap_buf, dtype=np_t))
+        a = _lib.Array()
+        a.data = self.data.data_ptr()
+        a.offset = self.view.offset
+        for i, d in enumerate(self.shape):
+            a.shape[i] = d
+        a.rank = len(self.shape)
+        a.dtype = self.dtype_code
+        return a
+
+    def copy_back(self):
+        if self.data is None:
+            return
+        vals = self.data.to("cpu").numpy().tolist()
+        if self.view.elem == "float":
+            vals = [float(v) for v in vals]
+        self.heap_buf[:] = vals

@@ -240,6 +240,7 @@ def main() -> None:
     from test_interp import ACCEL_SUM
     from test_acceptance import ALIAS_PROGRAM
     g["accel_sum"] = {str(w): run(ACCEL_SUM, mode="accel", workers=w) for w in (1, 2, 3, 8, 16)}
+    g["accel_sum"]["program"] = ACCEL_SUM
     g["alias"] = {str(w): run(ALIAS_PROGRAM, mode="accel", workers=w) for w in (1, 2, 8)}
     g["alias"]["program"] = ALIAS_PROGRAM
 
@@ -273,8 +274,89 @@ def main() -> None:
         src = MAPREDUCE.format(N=N)
         g["mapreduce"].append(dict(run(src, mode="accel", workers=W), N=N, workers=W, program=src))
 
+    g["adapter"] = record_adapter_constructs(CORPUS)
+
     out = HERE / "golden.json"
     out.write_text(json.dumps(g, indent=1, sort_keys=True))
+
+
+def record_adapter_constructs(corpus) -> dict:
+    """Run every corpus program in accel mode with the reference's own
+    skeletons, and for each device-context construct record the adapter's
+    translation of its function argument (lambda IR as JSON, with captured
+    host data), its inputs and the reference's result.  tests/test_gpu_adapter.py
+    replays each construct on the B200."""
+    import pmx.interp as interp
+    import pmx.runtime as rt
+    import pmx.syntax as syn
+    from paper_2211_00621_b200 import ir_json, pmx_adapter
+
+    orig = {n: getattr(interp, n) for n in ("eval_map", "eval_map2", "eval_reduce", "eval_loop")}
+    records: list = []
+
+    def conv(s):
+        return [ord(x) if isinstance(x, str) else (dict(x) if isinstance(x, dict) else x) for x in s]
+
+    def elem(s):
+        x = s[0] if s else 0
+        return "char" if isinstance(x, str) else ("bool" if isinstance(x, bool) else
+                                                  ("float" if isinstance(x, float) else
+                                                   ("record" if isinstance(x, dict) else "int")))
+
+    def translate(f, n, ctx, tensors):
+        def host_array(v):
+            if isinstance(v, rt.TensorView):
+                buf = ctx.heap.buffers[v.buffer]
+                h = ir_json.HostArray(list(buf), v.elem, v.shape, v.offset)
+                tensors.append((h, buf))
+                return h
+            return ir_json.HostArray(conv(v), elem(v))
+        try:
+            return ir_json.dump(pmx_adapter.to_lam(f, n, syn, rt, host_array))
+        except pmx_adapter.Unsupported:
+            return None
+
+    def rec(kind, ctx, f, arity, call, **kw):
+        tensors: list = []
+        lam = translate(f, arity, ctx, tensors) if ctx.run_parallel else None
+        out = call()
+        if lam is not None:
+            r = dict(kind=kind, lam=lam, expected=out if kind != "loop" else None, **kw)
+            if kind == "loop":
+                r["tensors_after"] = [list(buf) for _, buf in tensors]
+            records.append(r)
+        return out
+
+    def eval_map(f, s, ctx, span):
+        return rec("map", ctx, f, 1, lambda: orig["eval_map"](f, s, ctx, span), xs=conv(s), x_elem=elem(s)) \
+            if s else orig["eval_map"](f, s, ctx, span)
+
+    def eval_map2(f, s1, s2, ctx, span):
+        return rec("map2", ctx, f, 2, lambda: orig["eval_map2"](f, s1, s2, ctx, span), xs=conv(s1), ys=conv(s2),
+                   x_elem=elem(s1), y_elem=elem(s2)) if s1 else orig["eval_map2"](f, s1, s2, ctx, span)
+
+    def eval_reduce(f, acc, s, ctx, span):
+        return rec("reduce", ctx, f, 2, lambda: orig["eval_reduce"](f, acc, s, ctx, span), acc=acc, xs=conv(s),
+                   x_elem=elem(s)) if s else orig["eval_reduce"](f, acc, s, ctx, span)
+
+    def eval_loop(n, f, ctx, span):
+        return rec("loop", ctx, f, 1, lambda: orig["eval_loop"](n, f, ctx, span), n=n) \
+            if n > 0 else orig["eval_loop"](n, f, ctx, span)
+
+    out: dict = {}
+    interp.eval_map, interp.eval_map2, interp.eval_reduce, interp.eval_loop = eval_map, eval_map2, eval_reduce, eval_loop
+    try:
+        for name, src, rel in corpus:
+            records.clear()
+            try:
+                run_source(src, mode="accel", workers=4, capture_output=True)
+            except Diagnostics:
+                pass
+            out[name] = {"float_rel": rel, "constructs": list(records)}
+    finally:
+        for k, v in orig.items():
+            setattr(interp, k, v)
+    return out
     print(f"wrote {out}")
 
 

@@ -169,7 +169,7 @@ extern "C" {
 
 size_t pmx_knn_workspace_bytes(int64_t ntr, int64_t nq, int32_t d, int32_t k) {
     size_t base = (size_t)(ntr + nq) * sizeof(float) + 512;
-    if (knn_tc_eligible(d, k)) base += knn_tc_workspace(ntr, nq);
+    if (knn_tc_eligible(d, k)) base += knn_tc_workspace(ntr, nq) + 1024;
     return base;
 }
 
@@ -191,7 +191,8 @@ int pmx_knn_f32(const float* train, const int32_t* labels, int64_t ntr, const fl
     if (tc_path) {
         // bf16 operand copies + norms + exactness flag; the tensor-core kernels
         // run iff every coordinate is exact in bf16 (else the SIMT kernel does)
-        char* t = w + (size_t)(ntr + nq) * sizeof(float) + 512;
+        // tensor-core operand buffers: TMA needs 16-byte (we use 1 KiB) aligned bases
+        char* t = (char*)(((uintptr_t)(w + (size_t)(ntr + nq) * sizeof(float) + 512) + 1023) & ~(uintptr_t)1023);
         cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(unsigned), st);
         if (e != cudaSuccess) { set_last_error("knn flag: %s", cudaGetErrorString(e)); return -2; }
         int rc = knn_tc_run(train, query, labels, ntr, nq, k, ncls, out_label, out_idx, tnorm, qnorm, flag, t, st);

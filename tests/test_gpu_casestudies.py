@@ -127,7 +127,8 @@ def test_knn_golden(ix, golden):
     assert got.tolist() == [int(v) for v in e["stdout"].split()]
 
 
-@pytest.mark.parametrize("ntr,nq,d,k,c", [(5000, 300, 64, 8, 10), (1000, 130, 16, 3, 4), (777, 65, 64, 17, 10)])
+@pytest.mark.parametrize("ntr,nq,d,k,c", [(5000, 300, 64, 8, 10), (1000, 130, 16, 3, 4), (777, 65, 64, 17, 10),
+                                          (2000, 70, 64, 8, 10), (131, 257, 64, 1, 3), (4099, 513, 64, 5, 7)])
 def test_knn_vs_oracle(ntr, nq, d, k, c):
     X = synth.knn_train(ntr, d)
     Q = synth.knn_query(nq, d)

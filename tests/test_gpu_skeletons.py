@@ -85,7 +85,7 @@ def test_map2_matches_reference(case, golden):
 def test_accel_sum_schedule_independent(golden):
     # tests/test_interp.py:99-114 : reduce addi 0 (map (lam x. muli x x) [1..10]) = 385
     f = lambda s: eval_reduce(addi, 0, eval_map(lam("x", muli("x", "x")), s))
-    want = {int(v["stdout"]) for v in golden["accel_sum"].values()}
+    want = {int(v["stdout"]) for v in golden["accel_sum"].values() if isinstance(v, dict)}
     assert want == {385}
     for _ in range(20):
         assert accelerate(f, list(range(1, 11))) == 385

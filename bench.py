@@ -235,10 +235,9 @@ def bench_mapreduce(args, dist: Dist, peaks: dict) -> dict:
     e2e_body = lambda s: P.eval_reduce(P.addf, 0.0, P.eval_map(f, s))
 
     def e2e_step():
-        v = P.accelerate(e2e_body, host_x)
-        if dist.world > 1:
+        v = P.accelerate(e2e_body, host_x)        # this rank's shard: H2D + fused kernel + D2H
+        if dist.world > 1:                        # combine the per-rank partials (rank order)
             t = torch.tensor([v], dtype=torch.float64, device=dev)
-            prep.fold_partials(gathered) if False else None
             dist.pg.all_gather_into_tensor(gathered, t)
             return float(prep.fold_partials(gathered).item())
         return v

@@ -202,8 +202,19 @@ def bench_mapreduce(args, dist: Dist, peaks: dict) -> dict:
         dist.pg.all_gather_into_tensor(gathered, partial)
         return prep.fold_partials(gathered)           # fixed rank order (interp.py:334-336)
 
+    # N > 1: the shard partials are exchanged over NVLink peer memory by the
+    # reduce kernel itself (one launch per step, no collective); the NCCL
+    # all-gather + fold path is timed beside it as a variant.
+    peers = None
+    if dist.world > 1 and not args.nccl_combine:
+        from paper_2211_00621_b200.shard import PeerMailboxes
+        peers = PeerMailboxes()
+
     def step():
-        combine(prep.launch())
+        if peers is not None:
+            prep.launch_peers(peers)
+        else:
+            combine(prep.launch())
 
     launches0 = ctx.launches
     clocks = Clocks(torch.cuda.current_device())
@@ -211,7 +222,10 @@ def bench_mapreduce(args, dist: Dist, peaks: dict) -> dict:
     total_ms, per = device_time(step, args.steps, args.warmup, dist)
     clk = clocks.stop()
     launches = (ctx.launches - launches0) // (args.steps + args.warmup) * args.steps
-    result = float(combine(prep.launch()).item())
+    result = float((prep.launch_peers(peers) if peers is not None else combine(prep.launch())).item())
+    nccl_ms = None
+    if dist.world > 1:
+        nccl_ms, _ = device_time(lambda: combine(prep.launch()), args.steps, 1, dist)
     ctx.check_errors()
     exact = synth.mapreduce_exact_sum(n) if dist.world == 1 else None
 
@@ -257,7 +271,9 @@ def bench_mapreduce(args, dist: Dist, peaks: dict) -> dict:
                      "peak_source": peaks["source"]},
         "e2e": {"value": e2e_val, "unit": "elements/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 8,
                 "ms_per_step": e2e_ms / e2e_steps, "path": "accelerate(reduce addf 0.0 (map f s)) with pinned host s"},
-        "gpu_launches": launches + (args.steps if dist.world > 1 else 0),
+        "gpu_launches": launches,
+        "combine": ("peer-memory exchange fused into the reduce kernel (pmx_map_reduce_peers)" if peers is not None
+                    else ("NCCL all-gather + device fold" if dist.world > 1 else "single GPU")),
         "clocks": clk,
         "variants": {
             "map_only_8B": {"ms": map_ms / args.steps, "GB/s": 8 * n / (map_ms / args.steps * 1e-3) / 1e9,
@@ -268,6 +284,7 @@ def bench_mapreduce(args, dist: Dist, peaks: dict) -> dict:
                                            "GB/s": 8 * n / (mat_ms / args.steps * 1e-3) / 1e9,
                                            "frac": 8 * n / (mat_ms / args.steps * 1e-3) / 1e9 / peaks["hbm_gbs"]},
             "unfused_map_then_reduce_elem_per_s": n / ((map_ms + red_ms) / args.steps * 1e-3),
+            "nccl_allgather_combine_ms": (nccl_ms / args.steps) if nccl_ms is not None else None,
         },
     }
     return out
@@ -591,6 +608,8 @@ def main():
     ap.add_argument("--case", action="append", default=[])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baselines (quick experiments)")
+    ap.add_argument("--nccl-combine", action="store_true",
+                    help="N>1: combine reduce partials with NCCL all-gather instead of the fused peer kernel")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -69,7 +69,8 @@ enum pmx_code {
     PMX_E_TENSOR_OOB = 8,  /* "tensor index k out of bounds ..."  runtime.py:69-73 */
     PMX_E_NEVER = 9,       /* "reached a never expression"        interp.py:133-135 */
     PMX_E_F32_RANGE = 10,  /* result not representable in the f32 storage type */
-    PMX_E_SIN_COS_INF = 11 /* "sin/cos: math domain error" (inf argument)      */
+    PMX_E_SIN_COS_INF = 11,/* "sin/cos: math domain error" (inf argument)      */
+    PMX_E_PEER_TIMEOUT = 12/* a peer GPU did not deliver its partial (20 s)    */
 };
 
 /* ---- scalar-function bytecode ------------------------------------------
@@ -204,6 +205,39 @@ PMX_API int pmx_seq_loop(const pmx_program* f, double* state, double* scratch,
  *                                     replaces FlattenE interp.py:161-166 */
 PMX_API int pmx_scan_lengths(const int64_t* lengths, int64_t* offsets, int64_t n,
                      void* stream);
+
+/* ---- multi-GPU reduce: partials combined over NVLink peer memory ----------
+ * One process per GPU. Each rank creates a mailbox (pmx_peer_mailbox_create,
+ * zeroed, 512 B), exports its IPC handle, receives every peer's handle through
+ * the host's process group and maps them (pmx_peer_open). A pmx_peer_group
+ * then holds every rank's mailbox pointer (own pointer at [rank]).
+ * pmx_map_reduce_peers is pmx_map_reduce over this rank's shard whose last CTA
+ * also exchanges the shard partials through the mailboxes and folds the
+ * non-empty ones in rank order: `out` is the global result on every rank,
+ * from one kernel and no collective call. Each rank's shard folds from init
+ * (a reference chunk, interp.py:332-333); partials fold left in rank order
+ * (interp.py:334-336); empty shards are dropped (interp.py:276).
+ * `epoch` must be incremented (from 1) by every rank before each call; all
+ * ranks must make the same sequence of calls.       replaces eval_reduce's
+ * chunk combine across GPUs (interp.py:334-336) / an NCCL all-gather + fold. */
+#define PMX_MAX_PEERS 16
+#define PMX_IPC_HANDLE_BYTES 64
+typedef struct pmx_peer_group {
+    int32_t rank;
+    int32_t world;                       /* <= PMX_MAX_PEERS                  */
+    uint64_t epoch;                      /* >= 1, +1 per call                 */
+    uint64_t* mbox[PMX_MAX_PEERS];       /* device pointers, [rank] = own     */
+} pmx_peer_group;
+
+PMX_API int pmx_peer_mailbox_create(void** mbox_out, void* ipc_handle_out /* 64 B */);
+PMX_API int pmx_peer_mailbox_destroy(void* mbox);
+PMX_API int pmx_peer_open(const void* ipc_handle /* 64 B */, void** mbox_out);
+PMX_API int pmx_peer_close(void* mbox);
+PMX_API int pmx_map_reduce_peers(const pmx_program* f, const pmx_program* op,
+                   const void* x, int32_t x_dtype, int64_t n,
+                   const void* init_host, int32_t acc_dtype, void* out,
+                   void* workspace, size_t workspace_bytes,
+                   const pmx_peer_group* group, uint64_t* err, void* stream);
 
 /* ---- case-study kernels ---------------------------------------------------- */
 

@@ -44,7 +44,9 @@ ERROR_MESSAGES = {
     9: "reached a never expression (no pattern matched)",
     10: "value not representable in the f32 storage type",
     11: "math domain error",
+    12: "a peer GPU did not deliver its reduce partial (timeout)",
 }
+MAX_PEERS, IPC_HANDLE_BYTES = 16, 64
 
 
 class Insn(C.Structure):
@@ -64,6 +66,11 @@ class Program(C.Structure):
                 ("arrays", Array * MAX_ARRAYS)]
 
 
+class PeerGroup(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("epoch", C.c_uint64),
+                ("mbox", C.c_void_p * MAX_PEERS)]
+
+
 _lib = None
 _load_error: str | None = None
 
@@ -79,6 +86,12 @@ _SIGS = {
     "pmx_reduce_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "pmx_map_reduce": (C.c_int, [C.POINTER(Program), C.POINTER(Program), _P, C.c_int32, C.c_int64,
                                  _P, C.c_int32, _P, _P, C.c_int32, _P, C.c_size_t, _P, _P]),
+    "pmx_peer_mailbox_create": (C.c_int, [C.POINTER(C.c_void_p), _P]),
+    "pmx_peer_mailbox_destroy": (C.c_int, [_P]),
+    "pmx_peer_open": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    "pmx_peer_close": (C.c_int, [_P]),
+    "pmx_map_reduce_peers": (C.c_int, [C.POINTER(Program), C.POINTER(Program), _P, C.c_int32, C.c_int64,
+                                       _P, C.c_int32, _P, _P, C.c_size_t, C.POINTER(PeerGroup), _P, _P]),
     "pmx_fold": (C.c_int, [C.POINTER(Program), _P, C.c_int32, C.c_int64, _P, C.c_int32, _P,
                            _P, C.c_size_t, _P, _P]),
     "pmx_loop": (C.c_int, [C.POINTER(Program), C.c_int64, _P, _P]),

@@ -23,6 +23,7 @@
 #include <string.h>
 #include "common.cuh"
 #include "vm.cuh"
+#include "peer.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -246,10 +247,21 @@ __device__ __forceinline__ typename Op::A block_reduce(typename Op::A v) {
 
 // Last CTA to arrive folds the per-CTA partials in CTA order and applies init
 // once. Resets the ticket so the workspace can be reused on the stream.
+// With a peer group (pg.world > 0) the result is this rank's chunk partial;
+// warp 0 then exchanges it with the other GPUs over peer memory and writes
+// the rank-ordered fold of all chunk partials (peer.cuh).
+template <class Op>
+struct OpFold {
+    __device__ __forceinline__ typename Op::A operator()(typename Op::A a, typename Op::A b) const {
+        return Op::f(a, b);
+    }
+};
+
 template <class Op>
 __device__ __forceinline__ void grid_combine(typename Op::A block_total, typename Op::A* partials,
                                              unsigned* ticket, typename Op::A init,
-                                             typename Op::A* out) {
+                                             typename Op::A* out, const pmx_peer_group& pg,
+                                             int has, uint64_t* err) {
     typedef typename Op::A A;
     __shared__ bool s_last;
     if (threadIdx.x == 0) {
@@ -264,9 +276,21 @@ __device__ __forceinline__ void grid_combine(typename Op::A block_total, typenam
     A v = Op::id();
     for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) v = Op::f(v, __ldcg(&partials[i]));
     v = block_reduce<Op>(v);
-    if (threadIdx.x == 0) {
-        *out = Op::f(init, v);
-        *ticket = 0u;
+    if (pg.world == 0) {
+        if (threadIdx.x == 0) {
+            *out = Op::f(init, v);
+            *ticket = 0u;
+        }
+        return;
+    }
+    if (threadIdx.x < 32) {     // warp 0 holds v in every lane
+        bool ok;
+        int any;
+        A tot = peer_exchange<A>(pg, Op::f(init, v), has, OpFold<Op>(), Op::id(), err, &ok, &any);
+        if (threadIdx.x == 0) {
+            *out = any ? tot : init;
+            *ticket = 0u;
+        }
     }
 }
 
@@ -282,7 +306,7 @@ template <class T, class F, class Op, bool WRITE_Y, bool DO_REDUCE>
 __global__ void __launch_bounds__(256, WRITE_Y ? 8 : 4)
 k_map_reduce_vec(const T* __restrict__ x, T* __restrict__ y, int64_t n, F f,
                  typename Op::A* partials, unsigned* ticket, typename Op::A init,
-                 typename Op::A* out) {
+                 typename Op::A* out, const __grid_constant__ pmx_peer_group pg, uint64_t* err) {
     typedef typename Op::A A;
     constexpr int V = 16 / sizeof(T);     // elements per 128-bit packet
     constexpr int U = (WRITE_Y ? 16 : 32) / V;   // packets in flight per thread
@@ -337,7 +361,7 @@ k_map_reduce_vec(const T* __restrict__ x, T* __restrict__ y, int64_t n, F f,
     }
     if (DO_REDUCE) {
         A bt = block_reduce<Op>(Op::f(acc0, acc1));
-        grid_combine<Op>(bt, partials, ticket, init, out);
+        grid_combine<Op>(bt, partials, ticket, init, out, pg, n > 0, err);
     }
 }
 
@@ -346,7 +370,7 @@ template <class T, class F, class Op, bool WRITE_Y, bool DO_REDUCE>
 __global__ void __launch_bounds__(256)
 k_map_reduce_scalar(const T* __restrict__ x, T* __restrict__ y, int64_t n, F f,
                     typename Op::A* partials, unsigned* ticket, typename Op::A init,
-                    typename Op::A* out) {
+                    typename Op::A* out, const __grid_constant__ pmx_peer_group pg, uint64_t* err) {
     typedef typename Op::A A;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     A acc = Op::id();
@@ -357,7 +381,7 @@ k_map_reduce_scalar(const T* __restrict__ x, T* __restrict__ y, int64_t n, F f,
     }
     if (DO_REDUCE) {
         A bt = block_reduce<Op>(acc);
-        grid_combine<Op>(bt, partials, ticket, init, out);
+        grid_combine<Op>(bt, partials, ticket, init, out, pg, n > 0, err);
     }
 }
 
@@ -584,7 +608,10 @@ static int occupancy_grid(K kernel, int64_t work_items, int threads) {
 
 template <class T, class F, class Op, bool WY, bool RED>
 static int launch_mr(const T* x, T* y, int64_t n, F f, void* ws, typename Op::A init,
-                     typename Op::A* out, cudaStream_t st) {
+                     typename Op::A* out, cudaStream_t st, const pmx_peer_group* pgp = nullptr,
+                     uint64_t* err = nullptr) {
+    pmx_peer_group pg;
+    if (pgp) pg = *pgp; else memset(&pg, 0, sizeof(pg));
     const int V = 16 / sizeof(T);
     static int grid_cache[64] = {0};
     int dev = 0;
@@ -597,9 +624,9 @@ static int launch_mr(const T* x, T* y, int64_t n, F f, void* ws, typename Op::A 
     typename Op::A* partials = (typename Op::A*)((char*)ws + 256);
     bool aligned = ((uintptr_t)x % 16 == 0) && (!WY || (uintptr_t)y % 16 == 0);
     if (aligned)
-        k_map_reduce_vec<T, F, Op, WY, RED><<<grid, kReduceThreads, 0, st>>>(x, y, n, f, partials, ticket, init, out);
+        k_map_reduce_vec<T, F, Op, WY, RED><<<grid, kReduceThreads, 0, st>>>(x, y, n, f, partials, ticket, init, out, pg, err);
     else
-        k_map_reduce_scalar<T, F, Op, WY, RED><<<grid, kReduceThreads, 0, st>>>(x, y, n, f, partials, ticket, init, out);
+        k_map_reduce_scalar<T, F, Op, WY, RED><<<grid, kReduceThreads, 0, st>>>(x, y, n, f, partials, ticket, init, out, pg, err);
     PMX_CHECK_LAUNCH("map_reduce");
     return 0;
 }
@@ -607,13 +634,14 @@ static int launch_mr(const T* x, T* y, int64_t n, F f, void* ws, typename Op::A 
 // Dispatch on reduce operator for storage type T and functor F.
 template <class T, class F>
 static int dispatch_op(int okind, const T* x, T* y, int64_t n, F f, void* ws,
-                       const void* init_host, void* out, cudaStream_t st) {
+                       const void* init_host, void* out, cudaStream_t st,
+                       const pmx_peer_group* pg = nullptr, uint64_t* err = nullptr) {
     const bool wy = y != nullptr;
 #define PMX_MR(OP, ACC)                                                                        \
     {                                                                                          \
         ACC init; memcpy(&init, init_host, 8);                                                 \
-        return wy ? launch_mr<T, F, OP, true, true>(x, y, n, f, ws, init, (ACC*)out, st)       \
-                  : launch_mr<T, F, OP, false, true>(x, y, n, f, ws, init, (ACC*)out, st);     \
+        return wy ? launch_mr<T, F, OP, true, true>(x, y, n, f, ws, init, (ACC*)out, st, pg, err)  \
+                  : launch_mr<T, F, OP, false, true>(x, y, n, f, ws, init, (ACC*)out, st, pg, err); \
     }
     switch (okind) {
         case K_ADD_F: PMX_MR(OAddF, double)
@@ -635,6 +663,41 @@ static int dispatch_map_only(const T* x, T* y, int64_t n, F f, cudaStream_t st) 
 }
 
 static bool f32_exact(double v) { return (double)(float)v == v; }
+
+// Templated (recognised) path of map -> reduce; returns 1 when the program
+// pair has no templated kernel.
+static int map_reduce_fast(const pmx_program* f, const pmx_program* op, const void* x, int32_t xt,
+                           int64_t n, const void* init_host, int32_t acc_dtype, void* out,
+                           void* y, int32_t yt, void* ws, cudaStream_t st,
+                           const pmx_peer_group* pg, uint64_t* err) {
+    Affine A;
+    int fk = recognise_map(f, &A);
+    int ok = recognise_reduce(op);
+    const bool float_op = ok >= K_ADD_F && ok <= K_MAX_F;
+    const bool int_op = ok >= K_ADD_I && ok <= K_MAX_I;
+    const bool same_y = (y == nullptr) || (yt == xt);
+    if (!(same_y && ((float_op && acc_dtype == PMX_F64) || (int_op && acc_dtype == PMX_I64)))) return 1;
+    if (xt == PMX_F32 && float_op) {
+        if (fk == K_IDENTITY)
+            return dispatch_op<float>(ok, (const float*)x, (float*)y, n, FIdentity{}, ws, init_host, out, st, pg, err);
+        if (fk == K_AFFINE_F && f32_exact(A.af) && f32_exact(A.bf))
+            return dispatch_op<float>(ok, (const float*)x, (float*)y, n, FAffineF<float>{(float)A.af, (float)A.bf},
+                                      ws, init_host, out, st, pg, err);
+    } else if (xt == PMX_F64 && float_op) {
+        if (fk == K_IDENTITY)
+            return dispatch_op<double>(ok, (const double*)x, (double*)y, n, FIdentity{}, ws, init_host, out, st, pg, err);
+        if (fk == K_AFFINE_F)
+            return dispatch_op<double>(ok, (const double*)x, (double*)y, n, FAffineF<double>{A.af, A.bf},
+                                       ws, init_host, out, st, pg, err);
+    } else if (xt == PMX_I64 && int_op) {
+        if (fk == K_IDENTITY)
+            return dispatch_op<int64_t>(ok, (const int64_t*)x, (int64_t*)y, n, FIdentity{}, ws, init_host, out, st, pg, err);
+        if (fk == K_AFFINE_I)
+            return dispatch_op<int64_t>(ok, (const int64_t*)x, (int64_t*)y, n, FAffineI{A.ai, A.bi},
+                                        ws, init_host, out, st, pg, err);
+    }
+    return 1;
+}
 
 }  // namespace pmx
 
@@ -718,36 +781,8 @@ int pmx_map_reduce(const pmx_program* f, const pmx_program* op, const void* x, i
         return 0;
     }
     PMX_REQUIRE(ws && ws_bytes >= pmx_reduce_workspace_bytes(n), "pmx_map_reduce: workspace too small");
-    Affine A;
-    int fk = recognise_map(f, &A);
-    int ok = recognise_reduce(op);
-    const bool float_op = ok >= K_ADD_F && ok <= K_MAX_F;
-    const bool int_op = ok >= K_ADD_I && ok <= K_MAX_I;
-    const bool same_y = (y == nullptr) || (yt == xt);
-    if (same_y && ((float_op && acc_dtype == PMX_F64) || (int_op && acc_dtype == PMX_I64))) {
-        int r = 1;
-        if (xt == PMX_F32 && float_op) {
-            if (fk == K_IDENTITY)
-                r = dispatch_op<float>(ok, (const float*)x, (float*)y, n, FIdentity{}, ws, init_host, out, st);
-            else if (fk == K_AFFINE_F && f32_exact(A.af) && f32_exact(A.bf))
-                r = dispatch_op<float>(ok, (const float*)x, (float*)y, n,
-                                       FAffineF<float>{(float)A.af, (float)A.bf},
-                                       ws, init_host, out, st);
-        } else if (xt == PMX_F64 && float_op) {
-            if (fk == K_IDENTITY)
-                r = dispatch_op<double>(ok, (const double*)x, (double*)y, n, FIdentity{}, ws, init_host, out, st);
-            else if (fk == K_AFFINE_F)
-                r = dispatch_op<double>(ok, (const double*)x, (double*)y, n,
-                                        FAffineF<double>{A.af, A.bf}, ws, init_host, out, st);
-        } else if (xt == PMX_I64 && int_op) {
-            if (fk == K_IDENTITY)
-                r = dispatch_op<int64_t>(ok, (const int64_t*)x, (int64_t*)y, n, FIdentity{}, ws, init_host, out, st);
-            else if (fk == K_AFFINE_I)
-                r = dispatch_op<int64_t>(ok, (const int64_t*)x, (int64_t*)y, n,
-                                         FAffineI{A.ai, A.bi}, ws, init_host, out, st);
-        }
-        if (r <= 0) return r;
-    }
+    int r = map_reduce_fast(f, op, x, xt, n, init_host, acc_dtype, out, y, yt, ws, st, nullptr, err);
+    if (r <= 0) return r;
     // interpreter path
     int64_t init;
     memcpy(&init, init_host, 8);
@@ -760,6 +795,26 @@ int pmx_map_reduce(const pmx_program* f, const pmx_program* op, const void* x, i
                                           (int64_t*)out, y, yt, partials, ticket, err);
     PMX_CHECK_LAUNCH("map_reduce_vm");
     return 0;
+}
+
+int pmx_map_reduce_peers(const pmx_program* f, const pmx_program* op, const void* x, int32_t xt,
+                         int64_t n, const void* init_host, int32_t acc_dtype, void* out,
+                         void* ws, size_t ws_bytes, const pmx_peer_group* g, uint64_t* err, void* stream) {
+    PMX_REQUIRE(op && init_host && out && g, "pmx_map_reduce_peers: null argument");
+    PMX_REQUIRE(n >= 0, "pmx_map_reduce_peers: negative length");
+    PMX_REQUIRE(g->world >= 1 && g->world <= PMX_MAX_PEERS && g->rank >= 0 && g->rank < g->world,
+                "pmx_map_reduce_peers: bad group (rank %d of %d)", g->rank, g->world);
+    PMX_REQUIRE(g->epoch >= 1, "pmx_map_reduce_peers: epoch must start at 1");
+    for (int r = 0; r < g->world; ++r) PMX_REQUIRE(g->mbox[r], "pmx_map_reduce_peers: mailbox %d not mapped", r);
+    PMX_REQUIRE(ws && ws_bytes >= pmx_reduce_workspace_bytes(n), "pmx_map_reduce_peers: workspace too small");
+    PMX_REQUIRE(n == 0 || x, "pmx_map_reduce_peers: null input");
+    int r = map_reduce_fast(f, op, x, xt, n, init_host, acc_dtype, out, nullptr, xt, ws,
+                            (cudaStream_t)stream, g, err);
+    if (r == 1) {
+        set_last_error("pmx_map_reduce_peers: operator has no fused peer kernel (use the collective path)");
+        return -3;
+    }
+    return r;
 }
 
 int pmx_fold(const pmx_program* op, const void* x, int32_t xt, int64_t n,

@@ -69,6 +69,52 @@ def ordered_fold(partials: list, ranks: list[int], fold2: Callable):
     return total
 
 
+class PeerMailboxes:
+    """Every rank's reduce mailbox mapped into this process (CUDA IPC over
+    NVLink): the handles are exchanged once through the process group, after
+    which reduce partials move GPU to GPU inside the reduce kernel
+    (pmx_map_reduce_peers), with no collective call per reduction."""
+
+    def __init__(self):
+        import ctypes as C
+        from . import _lib
+        self.world, self.rank = world_rank()
+        lib = self.lib = _lib.load()
+        own = C.c_void_p()
+        handle = (C.c_uint8 * _lib.IPC_HANDLE_BYTES)()
+        _lib.check(lib.pmx_peer_mailbox_create(C.byref(own), handle), "peer mailbox")
+        self.own = own.value
+        handles = [bytes(handle)]
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(handle))
+        self.opened = []
+        self.group = _lib.PeerGroup()
+        self.group.rank, self.group.world, self.group.epoch = self.rank, self.world, 0
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.group.mbox[r] = self.own
+                continue
+            p = C.c_void_p()
+            buf = (C.c_uint8 * _lib.IPC_HANDLE_BYTES).from_buffer_copy(h)
+            _lib.check(lib.pmx_peer_open(buf, C.byref(p)), f"peer open (rank {r})")
+            self.group.mbox[r] = p.value
+            self.opened.append(p.value)
+
+    def next(self):
+        """The group for the next exchange (epoch + 1, same on every rank)."""
+        self.group.epoch += 1
+        return self.group
+
+    def close(self):
+        for p in self.opened:
+            self.lib.pmx_peer_close(p)
+        self.opened = []
+        if self.own:
+            self.lib.pmx_peer_mailbox_destroy(self.own)
+            self.own = None
+
+
 class ShardedMapReduce:
     """reduce op acc (map f s) over a sequence sharded across the ranks.
 
@@ -76,14 +122,19 @@ class ShardedMapReduce:
     `acc`, like each reference chunk), the per-rank partials are all-gathered
     (one NCCL call) and folded in rank order on the device."""
 
-    def __init__(self, f, op, acc, local_seq, n_global: int, ctx=None):
+    def __init__(self, f, op, acc, local_seq, n_global: int, ctx=None, peers: Optional[PeerMailboxes] = None):
         from .skeletons import PreparedMapReduce
         self.world, self.rank = world_rank()
         self.ranks = nonempty_ranks(n_global, self.world)
         self.prep = PreparedMapReduce(f, op, acc, local_seq, ctx)
         self.op = op
+        # fused peer-memory combine when the operator pair has a templated
+        # kernel and the mailboxes are mapped; else one all-gather + fold
+        self.peers = peers if (peers is not None and self.world > 1 and self.prep.has_peer_kernel()) else None
 
     def launch(self) -> torch.Tensor:
+        if self.peers is not None:
+            return self.prep.launch_peers(self.peers)   # one kernel: shard + exchange + fold
         part = self.prep.launch()                 # this shard (from acc)
         if self.world == 1:
             return part

@@ -413,6 +413,25 @@ class PreparedMapReduce:
         self.ctx.launches += 1
         return self.out
 
+    def launch_peers(self, group):
+        """This rank's shard reduced and combined with every other rank's
+        partial over NVLink peer memory in the same kernel (pmx_map_reduce_peers):
+        returns the global result (identical on every rank)."""
+        assert self.reduce and self.y is None
+        g = group.next()
+        rc = self.lib.pmx_map_reduce_peers(C.byref(self.f.program) if self.f is not None else None,
+                                           C.byref(self.op.program), self.s.ptr(), self.s.dtype_code,
+                                           self.s.numel, C.byref(self.init), self.code, self.out.data_ptr(),
+                                           self.ws.data_ptr(), self.ws.numel(), C.byref(g),
+                                           self.err.data_ptr(), self.ctx.stream_ptr())
+        _lib.check(rc, "map_reduce_peers")
+        self.ctx.launches += 1
+        return self.out
+
+    def has_peer_kernel(self) -> bool:
+        kf = 1 if self.f is None else self.lib.pmx_program_kind(C.byref(self.f.program), 0)
+        return kf in (1, 2, 3) and self.lib.pmx_program_kind(C.byref(self.op.program), 1) >= 10
+
     def fold_partials(self, partials):
         """Left fold of per-GPU partials in rank order (interp.py:334-336),
         on the device; `init` is not re-applied."""

@@ -206,6 +206,25 @@ PMX_API int pmx_seq_loop(const pmx_program* f, double* state, double* scratch,
 PMX_API int pmx_scan_lengths(const int64_t* lengths, int64_t* offsets, int64_t n,
                      void* stream);
 
+/* ---- run-time kernel specialisation ---------------------------------------
+ * A lambda the library does not recognise runs, above a size threshold, in
+ * the streaming skeleton kernel specialised to it: its bytecode is translated
+ * to C++ with the same semantics and compiled by NVRTC for sm_100a (cached per
+ * program shape; constants and captured arrays stay kernel arguments). Below
+ * the threshold (or with mode 0) it runs in the bytecode interpreter.
+ * mode: 0 = interpreter only, 1 = always specialise, 2 = auto (default; the
+ * PMX_JIT environment variable sets the initial mode). Returns the old mode. */
+PMX_API int pmx_jit_set_mode(int32_t mode);
+/* Kernels compiled / launched through the specialised path so far.          */
+PMX_API int pmx_jit_stats(int64_t* compiled, int64_t* launched);
+/* The generated element functor for skeleton kind 0 = map, 1 = map2,
+ * 2 = loop body (diagnostics); returns its length or < 0.                   */
+PMX_API int pmx_jit_source(const pmx_program* f, int32_t kind, char* buf, size_t len);
+/* Generate and compile (no GPU needed, nothing loaded) the kernel for kind
+ * with element dtypes x, y (map2: z = result dtype); 0 = compiles.          */
+PMX_API int pmx_jit_compile_check(const pmx_program* f, int32_t kind, int32_t x_dtype,
+                                  int32_t y_dtype, int32_t z_dtype);
+
 /* ---- multi-GPU reduce: partials combined over NVLink peer memory ----------
  * One process per GPU. Each rank creates a mailbox (pmx_peer_mailbox_create,
  * zeroed, 512 B), exports its IPC handle, receives every peer's handle through

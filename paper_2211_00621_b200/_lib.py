@@ -86,6 +86,10 @@ _SIGS = {
     "pmx_reduce_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "pmx_map_reduce": (C.c_int, [C.POINTER(Program), C.POINTER(Program), _P, C.c_int32, C.c_int64,
                                  _P, C.c_int32, _P, _P, C.c_int32, _P, C.c_size_t, _P, _P]),
+    "pmx_jit_set_mode": (C.c_int, [C.c_int32]),
+    "pmx_jit_stats": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "pmx_jit_source": (C.c_int, [C.POINTER(Program), C.c_int32, C.c_char_p, C.c_size_t]),
+    "pmx_jit_compile_check": (C.c_int, [C.POINTER(Program), C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "pmx_peer_mailbox_create": (C.c_int, [C.POINTER(C.c_void_p), _P]),
     "pmx_peer_mailbox_destroy": (C.c_int, [_P]),
     "pmx_peer_open": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
@@ -132,6 +136,13 @@ def load():
         raise RuntimeError("pmx B200 extension ABI mismatch")
     _lib = lib
     return lib
+
+
+def jit_stats() -> tuple[int, int]:
+    """(kernels compiled, launches) of the run-time specialised path."""
+    c, l = C.c_int64(), C.c_int64()
+    load().pmx_jit_stats(C.byref(c), C.byref(l))
+    return c.value, l.value
 
 
 def check(rc: int, what: str) -> None:

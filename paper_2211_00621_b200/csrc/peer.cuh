@@ -16,7 +16,7 @@
 // (it needs that peer's partial of the current epoch to finish), so the slot
 // it writes for epoch e+1 is never the one the peer is still reading for e.
 #pragma once
-#include "common.cuh"
+#include "device_common.cuh"
 
 namespace pmx {
 
@@ -43,6 +43,12 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     return t;
 }
 
+__device__ __forceinline__ uint64_t bits_of(double v) { return (uint64_t)__double_as_longlong(v); }
+__device__ __forceinline__ uint64_t bits_of(int64_t v) { return (uint64_t)v; }
+template <class A> __device__ __forceinline__ A from_bits(uint64_t b);
+template <> __device__ __forceinline__ double from_bits<double>(uint64_t b) { return __longlong_as_double((long long)b); }
+template <> __device__ __forceinline__ int64_t from_bits<int64_t>(uint64_t b) { return (int64_t)b; }
+
 __device__ __forceinline__ uint64_t* mbox_slot(uint64_t* mbox, uint64_t epoch, int src) {
     return mbox + ((int)(epoch & 1) * PMX_MAX_PEERS + src) * 2;
 }
@@ -55,8 +61,7 @@ template <class A, class Fold>
 __device__ A peer_exchange(const pmx_peer_group& g, A local, int has, Fold fold, A empty, uint64_t* err,
                            bool* ok, int* any_out) {
     const int lane = threadIdx.x & 31;
-    uint64_t bits;
-    memcpy(&bits, &local, 8);
+    const uint64_t bits = bits_of(local);
     const uint64_t flag = (g.epoch << 1) | (uint64_t)(has != 0);
     if (lane < g.world) {
         uint64_t* s = mbox_slot(g.mbox[lane], g.epoch, g.rank);
@@ -87,8 +92,7 @@ __device__ A peer_exchange(const pmx_peer_group& g, A local, int has, Fold fold,
         uint64_t vb = __shfl_sync(0xffffffffu, got, r);
         uint64_t fb = __shfl_sync(0xffffffffu, f, r);
         if (!(fb & 1)) continue;               // empty chunk: dropped (interp.py:276)
-        A v;
-        memcpy(&v, &vb, 8);
+        const A v = from_bits<A>(vb);
         total = any ? fold(total, v) : v;
         any = 1;
     }

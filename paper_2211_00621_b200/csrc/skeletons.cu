@@ -23,7 +23,8 @@
 #include <string.h>
 #include "common.cuh"
 #include "vm.cuh"
-#include "peer.cuh"
+#include "skel_kernels.cuh"
+#include "jit.h"
 
 namespace cg = cooperative_groups;
 
@@ -56,14 +57,7 @@ int sm_count() {
 // ------------------------------------------------------- program recognition
 // Fast-path kinds returned by pmx_program_kind (role 0 = unary map function
 // r0 = x, role 1 = binary reduce operator r0 = acc, r1 = x).
-enum FastKind {
-    K_VM = 0,
-    K_IDENTITY = 1,
-    K_AFFINE_F = 2,   // y = a*x + b (fp64 semantics; flags choose mul/add)
-    K_AFFINE_I = 3,   // y = a*x + b (int64 wrap)
-    K_ADD_F = 10, K_MUL_F = 11, K_MIN_F = 12, K_MAX_F = 13,
-    K_ADD_I = 20, K_MUL_I = 21, K_MIN_I = 22, K_MAX_I = 23,
-};
+// Fast-path kinds: enum FastKind in jit.h.
 
 struct Affine {
     double af, bf;       // float coefficients
@@ -163,227 +157,8 @@ static int recognise_reduce(const pmx_program* op) {
 }
 
 // ==================================================================== device
-// Streaming 128-bit load (read-only path, no L1 allocation). `volatile` keeps
-// the U loads of an unrolled iteration issued back to back before their use,
-// so every thread has U x 16 B in flight.
-__device__ __forceinline__ uint4 ldg_stream(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    return r;
-}
-__device__ __forceinline__ void stg_stream(void* p, uint4 v) {
-    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};"
-                 :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
-
-// ---- element functors (storage type T, compute type C) --------------------
-struct FIdentity {
-    template <class T> __device__ __forceinline__ T operator()(T x) const { return x; }
-};
-// y = a*x + b with each operation rounded separately, as CPython evaluates
-// `addf (mulf a x) b`.  `mulf a x` alone is a = a, b = -0.0 and `addf x b` is
-// a = 1.0: both identities are exact in IEEE arithmetic (signed zeros, NaN
-// and infinities included), so one branch-free functor covers all three.
-template <class C>
-struct FAffineF {
-    C a, b;
-    template <class T> __device__ __forceinline__ T operator()(T x) const {
-        return (T)add_rn(mul_rn(a, (C)x), b);
-    }
-    __device__ __forceinline__ static float mul_rn(float a, float b) { return __fmul_rn(a, b); }
-    __device__ __forceinline__ static float add_rn(float a, float b) { return __fadd_rn(a, b); }
-    __device__ __forceinline__ static double mul_rn(double a, double b) { return __dmul_rn(a, b); }
-    __device__ __forceinline__ static double add_rn(double a, double b) { return __dadd_rn(a, b); }
-};
-struct FAffineI {   // wrap-around a*x + b (a = 1 / b = 0 when absent: exact)
-    int64_t a, b;
-    __device__ __forceinline__ int64_t operator()(int64_t x) const { return wadd(wmul(a, x), b); }
-};
-
-// ---- reduce operators on the accumulator type ------------------------------
-struct OAddF { typedef double A; __device__ static double id() { return 0.0; }
-               __device__ static double f(double a, double b) { return __dadd_rn(a, b); } };
-struct OMulF { typedef double A; __device__ static double id() { return 1.0; }
-               __device__ static double f(double a, double b) { return __dmul_rn(a, b); } };
-struct OMinF { typedef double A; __device__ static double id() { return __longlong_as_double(0x7ff0000000000000ll); }
-               __device__ static double f(double a, double b) { return a < b ? a : b; } };
-struct OMaxF { typedef double A; __device__ static double id() { return __longlong_as_double(0xfff0000000000000ll); }
-               __device__ static double f(double a, double b) { return a > b ? a : b; } };
-struct OAddI { typedef int64_t A; __device__ static int64_t id() { return 0; }
-               __device__ static int64_t f(int64_t a, int64_t b) { return wadd(a, b); } };
-struct OMulI { typedef int64_t A; __device__ static int64_t id() { return 1; }
-               __device__ static int64_t f(int64_t a, int64_t b) { return wmul(a, b); } };
-struct OMinI { typedef int64_t A; __device__ static int64_t id() { return INT64_MAX; }
-               __device__ static int64_t f(int64_t a, int64_t b) { return a < b ? a : b; } };
-struct OMaxI { typedef int64_t A; __device__ static int64_t id() { return INT64_MIN; }
-               __device__ static int64_t f(int64_t a, int64_t b) { return a > b ? a : b; } };
-
-template <class Op>
-__device__ __forceinline__ typename Op::A warp_reduce(typename Op::A v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = Op::f(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-
-// Deterministic block reduction: XOR butterfly in each warp, then warp 0
-// folds the warp totals in warp order.
-template <class Op>
-__device__ __forceinline__ typename Op::A block_reduce(typename Op::A v) {
-    typedef typename Op::A A;
-    __shared__ A s_w[32];
-    v = warp_reduce<Op>(v);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) s_w[wid] = v;
-    __syncthreads();
-    const int nw = (blockDim.x + 31) >> 5;
-    if (wid == 0) {
-        v = lane < nw ? s_w[lane] : Op::id();
-        v = warp_reduce<Op>(v);
-    }
-    __syncthreads();
-    return v;   // valid in warp 0
-}
-
-// Last CTA to arrive folds the per-CTA partials in CTA order and applies init
-// once. Resets the ticket so the workspace can be reused on the stream.
-// With a peer group (pg.world > 0) the result is this rank's chunk partial;
-// warp 0 then exchanges it with the other GPUs over peer memory and writes
-// the rank-ordered fold of all chunk partials (peer.cuh).
-template <class Op>
-struct OpFold {
-    __device__ __forceinline__ typename Op::A operator()(typename Op::A a, typename Op::A b) const {
-        return Op::f(a, b);
-    }
-};
-
-template <class Op>
-__device__ __forceinline__ void grid_combine(typename Op::A block_total, typename Op::A* partials,
-                                             unsigned* ticket, typename Op::A init,
-                                             typename Op::A* out, const pmx_peer_group& pg,
-                                             int has, uint64_t* err) {
-    typedef typename Op::A A;
-    __shared__ bool s_last;
-    if (threadIdx.x == 0) {
-        partials[blockIdx.x] = block_total;
-        __threadfence();
-        unsigned t = atomicAdd(ticket, 1u);
-        s_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    A v = Op::id();
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) v = Op::f(v, __ldcg(&partials[i]));
-    v = block_reduce<Op>(v);
-    if (pg.world == 0) {
-        if (threadIdx.x == 0) {
-            *out = Op::f(init, v);
-            *ticket = 0u;
-        }
-        return;
-    }
-    if (threadIdx.x < 32) {     // warp 0 holds v in every lane
-        bool ok;
-        int any;
-        A tot = peer_exchange<A>(pg, Op::f(init, v), has, OpFold<Op>(), Op::id(), err, &ok, &any);
-        if (threadIdx.x == 0) {
-            *out = any ? tot : init;
-            *ticket = 0u;
-        }
-    }
-}
-
-// ---- vectorised fused map -> reduce (and plain map when Op is void) --------
-// T: storage type, F: functor on T, Op: reduce operator or NoReduce.
-struct NoReduce { typedef double A; __device__ static double id() { return 0.0; }
-                  __device__ static double f(double a, double) { return a; } };
-
-// Read-only streams (reductions) keep 128 B per thread in flight at 4 CTAs/SM
-// (measured 102% of the copy peak); read+write streams do better with more
-// resident warps and 64 B per thread (the stores add their own parallelism).
-template <class T, class F, class Op, bool WRITE_Y, bool DO_REDUCE>
-__global__ void __launch_bounds__(256, WRITE_Y ? 8 : 4)
-k_map_reduce_vec(const T* __restrict__ x, T* __restrict__ y, int64_t n, F f,
-                 typename Op::A* partials, unsigned* ticket, typename Op::A init,
-                 typename Op::A* out, const __grid_constant__ pmx_peer_group pg, uint64_t* err) {
-    typedef typename Op::A A;
-    constexpr int V = 16 / sizeof(T);     // elements per 128-bit packet
-    constexpr int U = (WRITE_Y ? 16 : 32) / V;   // packets in flight per thread
-    union P { uint4 u; T e[V]; };
-    const int64_t npk = n / V;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    A acc0 = Op::id(), acc1 = Op::id();   // two chains: halves the dependent-add depth
-    for (; p + (U - 1) * stride < npk; p += U * stride) {
-        P v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u].u = ldg_stream(x + (p + u * stride) * V);
-        // Join point on every loaded packet: a (never taken) branch on a value
-        // that depends on all U loads forces ptxas to issue all of them before
-        // any consumer, so U x 16 B per thread are in flight at once (it
-        // otherwise interleaves each load with the previous packet's use).
-        if (!WRITE_Y) {
-            unsigned j = 0;
-#pragma unroll
-            for (int u = 0; u < U; ++u) j += v[u].u.x;
-            if (j == 0x7fc00001u && n == -1) __trap();
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            P w;
-#pragma unroll
-            for (int e = 0; e < V; ++e) {
-                w.e[e] = f(v[u].e[e]);
-                if (DO_REDUCE) {
-                    if (e & 1) acc1 = Op::f(acc1, (A)w.e[e]);
-                    else acc0 = Op::f(acc0, (A)w.e[e]);
-                }
-            }
-            if (WRITE_Y) stg_stream(y + (p + u * stride) * V, w.u);
-        }
-    }
-    for (; p < npk; p += stride) {
-        P v, w;
-        v.u = ldg_stream(x + p * V);
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-            w.e[e] = f(v.e[e]);
-            if (DO_REDUCE) acc0 = Op::f(acc0, (A)w.e[e]);
-        }
-        if (WRITE_Y) stg_stream(y + p * V, w.u);
-    }
-    // scalar tail
-    for (int64_t j = npk * V + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-        T w = f(x[j]);
-        if (WRITE_Y) y[j] = w;
-        if (DO_REDUCE) acc0 = Op::f(acc0, (A)w);
-    }
-    if (DO_REDUCE) {
-        A bt = block_reduce<Op>(Op::f(acc0, acc1));
-        grid_combine<Op>(bt, partials, ticket, init, out, pg, n > 0, err);
-    }
-}
-
-// Scalar variant for misaligned views.
-template <class T, class F, class Op, bool WRITE_Y, bool DO_REDUCE>
-__global__ void __launch_bounds__(256)
-k_map_reduce_scalar(const T* __restrict__ x, T* __restrict__ y, int64_t n, F f,
-                    typename Op::A* partials, unsigned* ticket, typename Op::A init,
-                    typename Op::A* out, const __grid_constant__ pmx_peer_group pg, uint64_t* err) {
-    typedef typename Op::A A;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    A acc = Op::id();
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-        T w = f(x[j]);
-        if (WRITE_Y) y[j] = w;
-        if (DO_REDUCE) acc = Op::f(acc, (A)w);
-    }
-    if (DO_REDUCE) {
-        A bt = block_reduce<Op>(acc);
-        grid_combine<Op>(bt, partials, ticket, init, out, pg, n > 0, err);
-    }
-}
+// Streaming kernels (map / map2 / map->reduce / loop) live in skel_kernels.cuh,
+// shared with the run-time compiled instantiations (jit.cu).
 
 // ---- interpreter paths ------------------------------------------------------
 __global__ void k_map_vm(const __grid_constant__ pmx_program P, const void* x, int xt,
@@ -590,9 +365,16 @@ static inline int grid_for(int64_t work_items, int threads, int per_sm) {
     return (int)want;
 }
 
+// Grid of a streaming kernel over n elements: at least 8 four-element packets
+// per thread, at most one resident wave (`cap` CTAs).
+int stream_grid(int64_t n, int cap) {
+    int64_t want = (n / 4 + kStreamThreads * 8 - 1) / (kStreamThreads * 8);
+    if (want > cap) want = cap;
+    return (int)(want < 1 ? 1 : want);
+}
+
 // Workspace layout: [ticket u32 | pad to 256][partials: grid * 16 bytes]
-static const int kReduceThreads = 256;
-static const int kReduceBlocksPerSM = 8;
+static const int kReduceThreads = kStreamThreads;
 
 
 // One resident wave: grid = SMs x (CTAs per SM the kernel can hold), capped by
@@ -606,27 +388,25 @@ static int occupancy_grid(K kernel, int64_t work_items, int threads) {
     return grid_for(work_items, threads, per_sm);
 }
 
-template <class T, class F, class Op, bool WY, bool RED>
-static int launch_mr(const T* x, T* y, int64_t n, F f, void* ws, typename Op::A init,
+template <class TX, class TY, class F, class Op, bool WY, bool RED>
+static int launch_mr(const TX* x, TY* y, int64_t n, F f, void* ws, typename Op::A init,
                      typename Op::A* out, cudaStream_t st, const pmx_peer_group* pgp = nullptr,
                      uint64_t* err = nullptr) {
     pmx_peer_group pg;
     if (pgp) pg = *pgp; else memset(&pg, 0, sizeof(pg));
-    const int V = 16 / sizeof(T);
     static int grid_cache[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!grid_cache[dev & 63])
-        grid_cache[dev & 63] = occupancy_grid(k_map_reduce_vec<T, F, Op, WY, RED>, (int64_t)1 << 40, kReduceThreads);
-    int64_t want = (n / V + kReduceThreads * 8 - 1) / (kReduceThreads * 8);   // >= 8 packets per thread
-    int grid = (int)(want < grid_cache[dev & 63] ? (want < 1 ? 1 : want) : grid_cache[dev & 63]);
+        grid_cache[dev & 63] = occupancy_grid(k_map_reduce_vec<TX, TY, F, Op, WY, RED>, (int64_t)1 << 40, kReduceThreads);
+    int grid = stream_grid(n, grid_cache[dev & 63]);
     unsigned* ticket = (unsigned*)ws;
     typename Op::A* partials = (typename Op::A*)((char*)ws + 256);
-    bool aligned = ((uintptr_t)x % 16 == 0) && (!WY || (uintptr_t)y % 16 == 0);
+    bool aligned = ((uintptr_t)x % (4 * sizeof(TX)) == 0) && (!WY || (uintptr_t)y % (4 * sizeof(TY)) == 0);
     if (aligned)
-        k_map_reduce_vec<T, F, Op, WY, RED><<<grid, kReduceThreads, 0, st>>>(x, y, n, f, partials, ticket, init, out, pg, err);
+        k_map_reduce_vec<TX, TY, F, Op, WY, RED><<<grid, kReduceThreads, 0, st>>>(x, y, n, f, partials, ticket, init, out, pg, err);
     else
-        k_map_reduce_scalar<T, F, Op, WY, RED><<<grid, kReduceThreads, 0, st>>>(x, y, n, f, partials, ticket, init, out, pg, err);
+        k_map_reduce_scalar<TX, TY, F, Op, WY, RED><<<grid, kReduceThreads, 0, st>>>(x, y, n, f, partials, ticket, init, out, pg, err);
     PMX_CHECK_LAUNCH("map_reduce");
     return 0;
 }
@@ -637,11 +417,11 @@ static int dispatch_op(int okind, const T* x, T* y, int64_t n, F f, void* ws,
                        const void* init_host, void* out, cudaStream_t st,
                        const pmx_peer_group* pg = nullptr, uint64_t* err = nullptr) {
     const bool wy = y != nullptr;
-#define PMX_MR(OP, ACC)                                                                        \
-    {                                                                                          \
-        ACC init; memcpy(&init, init_host, 8);                                                 \
-        return wy ? launch_mr<T, F, OP, true, true>(x, y, n, f, ws, init, (ACC*)out, st, pg, err)  \
-                  : launch_mr<T, F, OP, false, true>(x, y, n, f, ws, init, (ACC*)out, st, pg, err); \
+#define PMX_MR(OP, ACC)                                                                              \
+    {                                                                                                \
+        ACC init; memcpy(&init, init_host, 8);                                                       \
+        return wy ? launch_mr<T, T, F, OP, true, true>(x, y, n, f, ws, init, (ACC*)out, st, pg, err)  \
+                  : launch_mr<T, T, F, OP, false, true>(x, y, n, f, ws, init, (ACC*)out, st, pg, err); \
     }
     switch (okind) {
         case K_ADD_F: PMX_MR(OAddF, double)
@@ -658,11 +438,10 @@ static int dispatch_op(int okind, const T* x, T* y, int64_t n, F f, void* ws,
 }
 
 template <class T, class F>
-static int dispatch_map_only(const T* x, T* y, int64_t n, F f, cudaStream_t st) {
-    return launch_mr<T, F, NoReduce, true, false>(x, y, n, f, nullptr, 0.0, nullptr, st);
+static int dispatch_map_only(const T* x, T* y, int64_t n, F f, cudaStream_t st, uint64_t* err) {
+    return launch_mr<T, T, F, NoReduce, true, false>(x, y, n, f, nullptr, 0.0, nullptr, st, nullptr, err);
 }
 
-static bool f32_exact(double v) { return (double)(float)v == v; }
 
 // Templated (recognised) path of map -> reduce; returns 1 when the program
 // pair has no templated kernel.
@@ -679,19 +458,19 @@ static int map_reduce_fast(const pmx_program* f, const pmx_program* op, const vo
     if (!(same_y && ((float_op && acc_dtype == PMX_F64) || (int_op && acc_dtype == PMX_I64)))) return 1;
     if (xt == PMX_F32 && float_op) {
         if (fk == K_IDENTITY)
-            return dispatch_op<float>(ok, (const float*)x, (float*)y, n, FIdentity{}, ws, init_host, out, st, pg, err);
-        if (fk == K_AFFINE_F && f32_exact(A.af) && f32_exact(A.bf))
-            return dispatch_op<float>(ok, (const float*)x, (float*)y, n, FAffineF<float>{(float)A.af, (float)A.bf},
+            return dispatch_op<float>(ok, (const float*)x, (float*)y, n, FIdentity<double>{}, ws, init_host, out, st, pg, err);
+        if (fk == K_AFFINE_F)
+            return dispatch_op<float>(ok, (const float*)x, (float*)y, n, FAffineF{A.af, A.bf},
                                       ws, init_host, out, st, pg, err);
     } else if (xt == PMX_F64 && float_op) {
         if (fk == K_IDENTITY)
-            return dispatch_op<double>(ok, (const double*)x, (double*)y, n, FIdentity{}, ws, init_host, out, st, pg, err);
+            return dispatch_op<double>(ok, (const double*)x, (double*)y, n, FIdentity<double>{}, ws, init_host, out, st, pg, err);
         if (fk == K_AFFINE_F)
-            return dispatch_op<double>(ok, (const double*)x, (double*)y, n, FAffineF<double>{A.af, A.bf},
+            return dispatch_op<double>(ok, (const double*)x, (double*)y, n, FAffineF{A.af, A.bf},
                                        ws, init_host, out, st, pg, err);
     } else if (xt == PMX_I64 && int_op) {
         if (fk == K_IDENTITY)
-            return dispatch_op<int64_t>(ok, (const int64_t*)x, (int64_t*)y, n, FIdentity{}, ws, init_host, out, st, pg, err);
+            return dispatch_op<int64_t>(ok, (const int64_t*)x, (int64_t*)y, n, FIdentity<int64_t>{}, ws, init_host, out, st, pg, err);
         if (fk == K_AFFINE_I)
             return dispatch_op<int64_t>(ok, (const int64_t*)x, (int64_t*)y, n, FAffineI{A.ai, A.bi},
                                         ws, init_host, out, st, pg, err);
@@ -740,17 +519,19 @@ int pmx_map(const pmx_program* f, const void* x, int32_t xt, void* y, int32_t yt
             if (e != cudaSuccess) { set_last_error("map copy: %s", cudaGetErrorString(e)); return -2; }
             return 0;
         }
-        if (kind == K_AFFINE_F && xt == PMX_F32 && f32_exact(A.af) && f32_exact(A.bf))
+        if (kind == K_AFFINE_F && xt == PMX_F32)
             return dispatch_map_only<float>((const float*)x, (float*)y, n,
-                                            FAffineF<float>{(float)A.af, (float)A.bf}, st);
+                                            FAffineF{A.af, A.bf}, st, err);
         if (kind == K_AFFINE_F && xt == PMX_F64)
             return dispatch_map_only<double>((const double*)x, (double*)y, n,
-                                             FAffineF<double>{A.af, A.bf}, st);
+                                             FAffineF{A.af, A.bf}, st, err);
         if (kind == K_AFFINE_I && xt == PMX_I64)
             return dispatch_map_only<int64_t>((const int64_t*)x, (int64_t*)y, n,
-                                              FAffineI{A.ai, A.bi}, st);
+                                              FAffineI{A.ai, A.bi}, st, err);
     }
     PMX_REQUIRE(f, "pmx_map: null program with differing dtypes");
+    int jr = jit_map(f, x, xt, y, yt, n, err, st);
+    if (jr <= 0) return jr;
     int grid = grid_for(n, 256, 8);
     k_map_vm<<<grid, 256, 0, st>>>(*f, x, xt, y, yt, n, err);
     PMX_CHECK_LAUNCH("map_vm");
@@ -762,6 +543,8 @@ int pmx_map2(const pmx_program* f, const void* x, int32_t xt, const void* y, int
     PMX_REQUIRE(n >= 0, "pmx_map2: negative length");
     if (n == 0) return 0;
     PMX_REQUIRE(f && x && y && z, "pmx_map2: null argument");
+    int jr = jit_map2(f, x, xt, y, yt, z, zt, n, err, (cudaStream_t)stream);
+    if (jr <= 0) return jr;
     int grid = grid_for(n, 256, 8);
     k_map2_vm<<<grid, 256, 0, (cudaStream_t)stream>>>(*f, x, xt, y, yt, z, zt, n, err);
     PMX_CHECK_LAUNCH("map2_vm");
@@ -783,6 +566,11 @@ int pmx_map_reduce(const pmx_program* f, const pmx_program* op, const void* x, i
     PMX_REQUIRE(ws && ws_bytes >= pmx_reduce_workspace_bytes(n), "pmx_map_reduce: workspace too small");
     int r = map_reduce_fast(f, op, x, xt, n, init_host, acc_dtype, out, y, yt, ws, st, nullptr, err);
     if (r <= 0) return r;
+    const int okind = recognise_reduce(op);
+    if (okind != K_VM && ((okind < K_ADD_I) == (acc_dtype == PMX_F64))) {
+        r = jit_map_reduce(f, okind, x, xt, n, init_host, out, y, yt, ws, st, nullptr, err);
+        if (r <= 0) return r;
+    }
     // interpreter path
     int64_t init;
     memcpy(&init, init_host, 8);
@@ -810,6 +598,9 @@ int pmx_map_reduce_peers(const pmx_program* f, const pmx_program* op, const void
     PMX_REQUIRE(n == 0 || x, "pmx_map_reduce_peers: null input");
     int r = map_reduce_fast(f, op, x, xt, n, init_host, acc_dtype, out, nullptr, xt, ws,
                             (cudaStream_t)stream, g, err);
+    const int okind = recognise_reduce(op);
+    if (r == 1 && okind != K_VM && ((okind < K_ADD_I) == (acc_dtype == PMX_F64)))
+        r = jit_map_reduce(f, okind, x, xt, n, init_host, out, nullptr, xt, ws, (cudaStream_t)stream, g, err);
     if (r == 1) {
         set_last_error("pmx_map_reduce_peers: operator has no fused peer kernel (use the collective path)");
         return -3;
@@ -838,6 +629,8 @@ int pmx_fold(const pmx_program* op, const void* x, int32_t xt, int64_t n,
 int pmx_loop(const pmx_program* body, int64_t n, uint64_t* err, void* stream) {
     PMX_REQUIRE(body, "pmx_loop: null body");
     if (n <= 0) return 0;    // interp.py:347-348
+    int jr = jit_loop(body, n, err, (cudaStream_t)stream);
+    if (jr <= 0) return jr;
     int grid = grid_for(n, 256, 8);
     k_loop_vm<<<grid, 256, 0, (cudaStream_t)stream>>>(*body, n, err);
     PMX_CHECK_LAUNCH("loop_vm");

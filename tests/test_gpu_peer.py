@@ -69,6 +69,10 @@ def _worker(rank, world, port, q):
         out["one"] = int(shard.ShardedMapReduce(None, P.addi, 1, se, 1, peers=peers).launch().item())
         sz = DeviceSeq(torch.empty(0, dtype=torch.int64).cuda(), (0,), _lib.PMX_I64)
         out["none"] = int(shard.ShardedMapReduce(None, P.addi, 5, sz, 0, peers=peers).launch().item())
+        # generic map (run-time specialised kernel) with the peer combine
+        sq = shard.ShardedMapReduce(P.lam("x", P.mulf("x", "x")), P.addf, 0.0, seq, n, peers=peers)
+        out["sq"] = float(sq.launch().item())
+        out["sq_local"] = float(sq.prep.launch().item())
         P.skeletons.default_ctx().check_errors()
         torch.cuda.synchronize()
         dist.barrier()
@@ -106,5 +110,6 @@ def test_peer_reduce_two_ranks_one_gpu():
     assert res[0]["max"] == res[1]["max"] == 7
     # empty chunk dropped: only rank 1's (1 + 41)
     assert res[0]["one"] == res[1]["one"] == 42
+    assert res[0]["sq"] == res[1]["sq"] == res[0]["sq_local"] + res[1]["sq_local"]
     # all chunks empty: reduce over [] returns acc
     assert res[0]["none"] == res[1]["none"] == 5

@@ -17,6 +17,17 @@ from paper_2211_00621_b200 import (
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(params=[0, 1], ids=["vm", "jit"], autouse=True)
+def jit_mode(request):
+    """Every case runs twice: bytecode interpreter only, and always through
+    the run-time specialised kernels (csrc/jit.cu)."""
+    from paper_2211_00621_b200 import _lib
+    lib = _lib.load()
+    prev = lib.pmx_jit_set_mode(request.param)
+    yield request.param
+    lib.pmx_jit_set_mode(prev)
+
 TRANSCENDENTAL = {"exp", "log", "sin_cos", "float_math"}
 
 

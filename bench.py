@@ -240,6 +240,7 @@ def bench_mapreduce(args, dist: Dist, peaks: dict) -> dict:
     mat_ms, _ = device_time(prep_mat.launch, args.steps, 1, dist)
     ctx.check_errors()
 
+    generic = bench_generic_skeletons(x, n, args, dist, peaks)
     kern_ms = statistics.mean(per)
     bytes_per_launch = 4 * n
     achieved = bytes_per_launch / (kern_ms * 1e-3) / 1e9
@@ -285,8 +286,43 @@ def bench_mapreduce(args, dist: Dist, peaks: dict) -> dict:
                                            "frac": 8 * n / (mat_ms / args.steps * 1e-3) / 1e9 / peaks["hbm_gbs"]},
             "unfused_map_then_reduce_elem_per_s": n / ((map_ms + red_ms) / args.steps * 1e-3),
             "nccl_allgather_combine_ms": (nccl_ms / args.steps) if nccl_ms is not None else None,
+            "generic_lambdas": generic,
         },
     }
+    return out
+
+
+def bench_generic_skeletons(x, n, args, dist, peaks) -> dict:
+    """The skeletons on lambdas the library does not recognise (run-time
+    specialised kernels, csrc/jit.cu) over the same 2^28 fp32 shard:
+    map / map2 / map->reduce / loop, HBM roofline each."""
+    import torch
+    import paper_2211_00621_b200 as P
+    from paper_2211_00621_b200 import _lib
+    from paper_2211_00621_b200.runtime import DeviceSeq, DeviceTensor, _Root
+    xs = DeviceSeq(x, (n,), _lib.PMX_F32)
+    ys = DeviceSeq(torch.roll(x, 1), (n,), _lib.PMX_F32)
+    yt = torch.empty_like(x)
+    tx = DeviceTensor(_Root(x, 0, 0, n, _lib.PMX_F32), 0, (n,), "float")
+    ty = DeviceTensor(_Root(yt, 1, 0, n, _lib.PMX_F32), 0, (n,), "float")
+    f = P.lam("x", P.addf(P.mulf("x", "x"), 1.0))
+    g = P.lam("a", "b", P.subf(P.mulf("a", "b"), "a"))
+    sq = P.lam("x", P.mulf("x", "x"))
+    body = P.lam("i", P.tensor_set(ty, ["i"], P.addf(P.mulf(2.0, P.tensor_get(tx, ["i"])), 1.0)))
+    cases = [("map (lam x. x*x + 1)", lambda: P.eval_map(f, xs).materialize(), 8),
+             ("map2 (lam a b. a*b - a)", lambda: P.eval_map2(g, xs, ys), 12),
+             ("reduce addf 0.0 (map (lam x. x*x))", lambda: P.eval_reduce(P.addf, 0.0, P.eval_map(sq, xs)), 4),
+             ("loop n (lam i. tensorSet y [i] (2*(tensorGet x [i])+1))", lambda: P.eval_loop(n, body), 8)]
+    out = {}
+    c0, l0 = _lib.jit_stats()
+    for name, fn, bpe in cases:
+        ms, _ = device_time(fn, args.steps, 3, dist)
+        ms /= args.steps
+        gbs = bpe * n / (ms * 1e-3) / 1e9
+        out[name] = {"ms": round(ms, 4), "bytes_per_elem": bpe, "GB/s": round(gbs, 1),
+                     "frac": round(gbs / peaks["hbm_gbs"], 3), "elem_per_s": n / (ms * 1e-3)}
+    c1, l1 = _lib.jit_stats()
+    out["_jit"] = {"kernels_compiled": c1 - c0, "launches": l1 - l0}
     return out
 
 

@@ -267,7 +267,7 @@ def bench_mapreduce(args, dist: Dist, peaks: dict) -> dict:
         "result": result, "exact_result": exact, "result_exact_match": (result == exact) if exact else None,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _traffic_from_profiles(),
-                     "kernel": "k_map_reduce_vec<float,FAffineF<float>,OAddF,false,true>",
+                     "kernel": "k_map_reduce_vec<float,float,FAffineF,OAddF,false,true> (fp64 map + sum, Float semantics)",
                      "bytes_per_launch": bytes_per_launch, "kernel_ms": round(kern_ms, 5),
                      "peak_source": peaks["source"]},
         "e2e": {"value": e2e_val, "unit": "elements/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 8,
@@ -469,18 +469,22 @@ def bench_hmm(args, dist, peaks) -> dict:
     total, per = device_time(step, s, w, dist)
     ms = total / s
     flops = 2.0 * S * S * (T - 1) * nsig
-    return {"config": "4096 signals x 10^4 steps x 1024 states, K=8, fp32 trellis + fp64 log-scale",
+    smem_step = 2 * 2 * S * S + (S // 128) * S * 32 * 2      # A^T write + read (fp16) + B re-reads
+    return {"config": "4096 signals x 10^4 steps x 1024 states, K=8, fp16 operands / fp32 accumulate + fp64 log-scale",
             "element": "signal", "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms,
             "steps": s, "warmup": w,
             "roofline": {"bound": "shared memory (A^T streamed through smem every step)",
                          "achieved_tflops": flops / (ms * 1e-3) / 1e12,
-                         "peak_tflops": peaks["bf16_tflops"] / 2,
-                         "peak_source": "tf32 dense = 1/2 of measured bf16",
-                         "frac": flops / (ms * 1e-3) / 1e12 / (peaks["bf16_tflops"] / 2),
-                         "smem_bytes_per_sm_per_step": 2 * 4 * S * S + 4 * S * 32,
-                         "smem_B_per_clk_per_sm": (2 * 4 * S * S + 4 * S * 32) * (T - 1) / (ms * 1e-3) / 1.965e9,
-                         "note": "tcgen05 kind::tf32 (RNA-rounded operands), 32 signals per CTA, TMA multicast "
-                                 "of A^T tiles across 4-CTA clusters, fp64 log-scale"},
+                         "peak_tflops": peaks["bf16_tflops"],
+                         "peak_source": "f16 dense = measured bf16 dense (MEASURED_PEAKS.json)",
+                         "frac": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                         "smem_bytes_per_sm_per_step": smem_step,
+                         "smem_B_per_clk_per_sm": smem_step * (T - 1) / (ms * 1e-3) / 1.965e9,
+                         "smem_frac": smem_step * (T - 1) / (ms * 1e-3) / 1.965e9 / 128.0,
+                         "note": "tcgen05 kind::f16 (2^10-scaled fp16 operands, fp32 TMEM accumulation), 32 signals "
+                                 "per CTA, TMA multicast of A^T tiles across 4-CTA clusters, fp64 log-scale; per step "
+                                 "every SM writes (TMA) + reads (UMMA) the 2 MiB A^T and re-reads 512 KiB of u: "
+                                 "smem_frac is that traffic against 128 B/clk/SM"},
             "_ll": out.to("cpu").numpy()}
 
 

@@ -40,6 +40,23 @@ def mapreduce(reps=3):
     torch.cuda.synchronize()
 
 
+def generic(reps=2):
+    """Run-time specialised kernels (jit.cu): map / loop on unrecognised lambdas."""
+    from paper_2211_00621_b200.runtime import DeviceTensor, _Root
+    n = 1 << 28
+    x = synth.mapreduce_x_device(n, torch.device("cuda"))
+    xs = DeviceSeq(x, (n,), _lib.PMX_F32)
+    yt = torch.empty_like(x)
+    tx = DeviceTensor(_Root(x, 0, 0, n, _lib.PMX_F32), 0, (n,), "float")
+    ty = DeviceTensor(_Root(yt, 1, 0, n, _lib.PMX_F32), 0, (n,), "float")
+    f = P.lam("x", P.addf(P.mulf("x", "x"), 1.0))
+    body = P.lam("i", P.tensor_set(ty, ["i"], P.addf(P.mulf(2.0, P.tensor_get(tx, ["i"])), 1.0)))
+    for _ in range(reps):
+        P.eval_map(f, xs).materialize()
+        P.eval_loop(n, body)
+    torch.cuda.synchronize()
+
+
 def rk4(reps=2):
     ps = torch.from_numpy(synth.rk4_params(10_000)).cuda()
     s0 = torch.from_numpy(synth.RK4_INIT).cuda()

@@ -508,6 +508,63 @@ def cpu_hmm(seconds=10.0) -> dict:
             "sample": f"{reps}x {obs.shape[0]} signals x {T} steps at S=1024 (log-space oracle), scaled to T=10^4"}
 
 
+def bench_viterbi(args, dist, peaks) -> dict:
+    """Viterbi decoding (programs/viterbi.pmx) at scale: SURVEY §8(f) rank 1.
+    Not a BASELINE config: the HMM model of the forward config (S=1024, K=8),
+    1184 signals (8 per SM) x T=1000, fp64 like the reference."""
+    import numpy as np
+    import torch
+    from paper_2211_00621_b200 import _lib, synth
+    S, K, nsig, T = 1024, 8, 148 * 8, 1000
+    dev = torch.device("cuda", torch.cuda.current_device())
+    A, E, pi = synth.hmm_model(S, K)
+    lA = torch.from_numpy(np.log(A)).to(dev)
+    lE = torch.from_numpy(np.log(E)).to(dev)
+    lpi = torch.from_numpy(np.log(pi)).to(dev)
+    obs = torch.from_numpy(synth.hmm_obs(nsig, T, K)).to(dev)
+    path = torch.empty(nsig * T, dtype=torch.int32, device=dev)
+    logp = torch.empty(nsig, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    ws = torch.empty(lib.pmx_viterbi_workspace_bytes(S, nsig, T), dtype=torch.uint8, device=dev)
+
+    def step():
+        _lib.check(lib.pmx_viterbi_f64(lpi.data_ptr(), lA.data_ptr(), lE.data_ptr(), S, K, obs.data_ptr(), nsig,
+                                       T, path.data_ptr(), logp.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       torch.cuda.current_stream().cuda_stream), "viterbi")
+    w, s = min(args.warmup, 1), max(1, min(args.steps, 2))
+    total, per = device_time(step, s, w, dist)
+    ms = total / s
+    cells = float(S) * S * (T - 1) * nsig
+    fp64_lanes = 64.0 * 148 * 1.965e9          # FP64 lanes/s (B200: 64 per SM per clock)
+    return {"config": f"S={S}, K={K}, {nsig} signals x T={T}, fp64 (viterbi.pmx semantics)", "element": "signal",
+            "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms, "steps": s, "warmup": w,
+            "cells_per_s": cells / (ms * 1e-3),
+            "roofline": {"bound": "FP64 pipe (DADD + DSETP per max-plus cell)",
+                         "achieved_fp64_ops_per_s": 2 * cells / (ms * 1e-3), "peak_fp64_ops_per_s": fp64_lanes,
+                         "frac": 2 * cells / (ms * 1e-3) / fp64_lanes,
+                         "peak_source": "64 FP64 lanes/clk/SM x 148 SMs x 1.965 GHz (B200 FP64 40 TFLOP/s)"},
+            "_path": path}
+
+
+def cpu_viterbi(seconds=10.0) -> dict:
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    from paper_2211_00621_b200 import synth
+    th = cpu_threads()
+    A, E, pi = synth.hmm_model(1024, 8)
+    T = 20
+    obs = synth.hmm_obs(max(2, th), T, 8)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.viterbi(A, E, pi, obs, threads=th)
+        reps += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": obs.shape[0] * (T - 1) / dt / (1000 - 1), "unit": "signals/s (T=1000 equivalent)",
+            "cores": th, "kind": "port", "sample": f"{reps}x {obs.shape[0]} signals x {T} steps at S=1024"}
+
+
 def bench_kmer(args, dist, peaks) -> dict:
     import numpy as np
     import torch
@@ -571,7 +628,8 @@ def run_ours(args):
     case = {}
     if not args.no_case_studies:
         for name, fn, cfn in (("rk4", bench_rk4, cpu_rk4), ("knn", bench_knn, cpu_knn),
-                              ("hmm_forward", bench_hmm, cpu_hmm), ("hmm_kmer", bench_kmer, cpu_kmer)):
+                              ("hmm_forward", bench_hmm, cpu_hmm), ("hmm_kmer", bench_kmer, cpu_kmer),
+                              ("viterbi", bench_viterbi, cpu_viterbi)):
             if args.case and name not in args.case:
                 continue
             try:

@@ -116,6 +116,17 @@ def test_viterbi_vs_oracle():
     assert np.allclose(r["logp"], logp, rtol=1e-12)
 
 
+@pytest.mark.parametrize("S,nsig,T", [(256, 37, 60), (512, 21, 40), (1024, 11, 30), (1024, 9, 1)])
+def test_viterbi_tiled_vs_oracle(S, nsig, T):
+    # batched register-tiled kernel (viterbi.cu): paths bit-exact, logp fp64
+    A, E, pi = synth.hmm_model(S, 8)
+    obs = synth.hmm_obs(nsig, T, 8)
+    r = accelerate(viterbi, A, E, pi, obs)
+    path, logp = O.viterbi(A, E, pi, obs)
+    assert np.array_equal(np.asarray(r["path"]).reshape(nsig, T), path)
+    assert np.allclose(np.asarray(r["logp"]), logp, rtol=1e-12, atol=0)
+
+
 # ------------------------------------------------------------------ k-NN
 @pytest.mark.parametrize("ix", [0, 1, 2])
 def test_knn_golden(ix, golden):

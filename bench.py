@@ -539,10 +539,12 @@ def bench_viterbi(args, dist, peaks) -> dict:
     return {"config": f"S={S}, K={K}, {nsig} signals x T={T}, fp64 (viterbi.pmx semantics)", "element": "signal",
             "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms, "steps": s, "warmup": w,
             "cells_per_s": cells / (ms * 1e-3),
-            "roofline": {"bound": "FP64 pipe (DADD + DSETP per max-plus cell)",
+            "roofline": {"bound": "issue (5 SASS instr per max-plus cell: DADD, DSETP, 3 selects) / FP64 pipe",
                          "achieved_fp64_ops_per_s": 2 * cells / (ms * 1e-3), "peak_fp64_ops_per_s": fp64_lanes,
                          "frac": 2 * cells / (ms * 1e-3) / fp64_lanes,
-                         "peak_source": "64 FP64 lanes/clk/SM x 148 SMs x 1.965 GHz (B200 FP64 40 TFLOP/s)"},
+                         "issue_frac": 5 * cells / (ms * 1e-3) / (128.0 * 148 * 1.965e9),
+                         "peak_source": "64 FP64 lanes/clk/SM x 148 SMs x 1.965 GHz (B200 FP64 40 TFLOP/s); "
+                                        "issue: 4 x 32 thread-instr/clk/SM"},
             "_path": path}
 
 

@@ -280,9 +280,10 @@ __global__ void k_viterbi(const double* __restrict__ log_pi, const double* __res
 }
 
 bool viterbi_tiled_eligible(int S);
+size_t viterbi_tiled_workspace(int S, int64_t nsig, int T);
 int viterbi_tiled_launch(const double* log_pi, const double* log_A, const double* log_E, int S, int K,
-                         const int* obs, int64_t nsig, int T, int* path, double* logp, int* back,
-                         double* chi_final, cudaStream_t st);
+                         const int* obs, int64_t nsig, int T, int* path, double* logp, void* ws,
+                         cudaStream_t st);
 size_t hmm_tc_workspace(int S, int K);
 bool hmm_tc_eligible(int S, int K);
 int hmm_tc_launch(const float* log_pi, const float* A, const float* log_E, int S, int K, const int* obs,
@@ -343,9 +344,11 @@ int pmx_hmm_forward_f32(const float* log_pi, const float* A, const float* log_E,
 }
 
 size_t pmx_viterbi_workspace_bytes(int32_t S, int64_t nsig, int32_t T) {
-    // back pointers [nsig][T-1][S] int32 | final chi [nsig][S] fp64 (tiled path)
-    const size_t bp = ((size_t)nsig * (size_t)(T > 1 ? T - 1 : 0) * (size_t)S * sizeof(int32_t) + 255) & ~(size_t)255;
-    return bp + (size_t)nsig * (size_t)S * sizeof(double) + 256;
+    // simple kernel: back pointers [nsig][T-1][S] int32; tiled kernels (S in
+    // {256, 512, 1024}): chi history / back pointers + final chi + log A^T
+    const size_t simple = (size_t)nsig * (size_t)(T > 1 ? T - 1 : 0) * (size_t)S * sizeof(int32_t) + 256;
+    const size_t tiled = viterbi_tiled_eligible(S) ? viterbi_tiled_workspace(S, nsig, T) : 0;
+    return simple > tiled ? simple : tiled;
 }
 
 int pmx_viterbi_f64(const double* log_pi, const double* log_A, const double* log_E, int32_t S, int32_t K,
@@ -357,12 +360,9 @@ int pmx_viterbi_f64(const double* log_pi, const double* log_A, const double* log
     // S in {256, 512, 1024}: batched register-tiled kernel (viterbi.cu);
     // PMX_VITERBI_SIMPLE=1 forces the one-CTA-per-signal kernel (A/B checks)
     static const bool simple = getenv("PMX_VITERBI_SIMPLE") && getenv("PMX_VITERBI_SIMPLE")[0] == '1';
-    if (!simple && viterbi_tiled_eligible(S)) {
-        const size_t bp = ((size_t)nsig * (size_t)(T > 1 ? T - 1 : 0) * (size_t)S * sizeof(int32_t) + 255) &
-                          ~(size_t)255;
-        return viterbi_tiled_launch(log_pi, log_A, log_E, S, K, obs, nsig, T, path, logp, (int*)ws,
-                                    (double*)((char*)ws + bp), (cudaStream_t)stream);
-    }
+    if (!simple && viterbi_tiled_eligible(S))
+        return viterbi_tiled_launch(log_pi, log_A, log_E, S, K, obs, nsig, T, path, logp, ws,
+                                    (cudaStream_t)stream);
     const size_t smem = 2 * (size_t)S * sizeof(double);
     PMX_REQUIRE(smem <= 200 * 1024, "pmx_viterbi_f64: S too large");
     if (smem > 48 * 1024)

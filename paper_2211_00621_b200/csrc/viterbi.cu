@@ -19,10 +19,13 @@
 // buffer of KT rows (A is step-invariant, so the buffer prefetches across
 // steps); each thread keeps a 4-signal x 8-state tile of (best score, argmax)
 // in registers, so one A row chunk and one chi chunk feed 32 max-plus cells.
-// Per cell: one DADD + one DSETP (FP64 pipe) + two selects: the kernel is
-// FP64-pipe bound (64 lanes/clk/SM => 32 cells/clk/SM).
+// Per cell: one DADD + one DSETP (FP64 pipe) + three selects (SASS: DADD,
+// DSETP.GT, 2x FSEL, SEL) — five issue slots per cell, so the kernel is
+// issue-bound at <= 25.6 cells/clk/SM (4 schedulers x 32 lanes / 5) before
+// the FP64 pipe's 32 cells/clk/SM (64 lanes, 2 FP64 ops per cell).
 // Back pointers go to the caller's workspace [nsig][T-1][S] int32; a second
 // kernel (one warp per signal) takes the final argmax and walks them back.
+#include <stdlib.h>
 #include "common.cuh"
 
 namespace pmx {
@@ -46,11 +49,18 @@ __device__ __forceinline__ void vt_load_stage(double* dst, const double* __restr
     for (int v = threadIdx.x; v < VEC; v += VT_NT) vt_cp_async16(dst + v * 2, src + v * 2);
 }
 
-template <int S>
+// ARGMAX = true: (score, argmax) per cell in registers, back pointers stored
+// [nsig][T-1][S] int32 (DADD + DSETP + 3 selects per cell: issue-bound).
+// ARGMAX = false: scores only (DADD + DMNMX per cell) and the chi vectors of
+// every step stored [nsig][T-1][S] fp64; the backtrack recomputes the one
+// argmax per step it needs (viterbi.pmx's back pointer for the state on the
+// path) from chi_{t-1} and a column of log A — bit-identical scores, 1/S of
+// the forward work.
+template <int S, bool ARGMAX>
 __global__ void __launch_bounds__(VT_NT, 1)
 k_viterbi_tiled(const double* __restrict__ log_pi, const double* __restrict__ log_A,
                 const double* __restrict__ log_E, int K, const int* __restrict__ obs, int64_t nsig, int T,
-                int* __restrict__ back, double* __restrict__ chi_out) {
+                int* __restrict__ back, double* __restrict__ hist, double* __restrict__ chi_out) {
     constexpr int GT = S / 8;              // threads per signal group (8 states each)
     constexpr int NG = VT_NT / GT;         // signal groups
     constexpr int MS = NG * 4;             // signals per CTA
@@ -72,6 +82,7 @@ k_viterbi_tiled(const double* __restrict__ log_pi, const double* __restrict__ lo
         const int64_t sig = s0 + m;
         const int o = sig < nsig ? obs[sig * T] : 0;
         chiT[v] = __dadd_rn(log_pi[i], log_E[(int64_t)i * K + o]);
+        if (!ARGMAX && T > 1 && sig < nsig) hist[sig * steps * S + i] = chiT[v];
     }
     if (T > 1) { vt_load_stage<S>(As, log_A, 0); vt_commit(); }
     __syncthreads();
@@ -115,7 +126,11 @@ k_viterbi_tiled(const double* __restrict__ log_pi, const double* __restrict__ lo
 #pragma unroll
                     for (int y = 0; y < 8; ++y) {
                         const double sc = __dadd_rn(av[x], bv[y]);
-                        if (sc > best[x][y]) { best[x][y] = sc; arg[x][y] = k; }   // first max wins
+                        if (ARGMAX) {
+                            if (sc > best[x][y]) { best[x][y] = sc; arg[x][y] = k; }   // first max wins
+                        } else {
+                            best[x][y] = fmax(best[x][y], sc);
+                        }
                     }
             }
             __syncthreads();   // stage buffer (and, at the last kt, chiT) reads complete
@@ -132,9 +147,16 @@ k_viterbi_tiled(const double* __restrict__ log_pi, const double* __restrict__ lo
                 const int j = y < 4 ? j0 + y : j1 + y - 4;
                 best[x][y] = __dadd_rn(best[x][y], __ldg(log_E + (int64_t)j * K + o));
             }
-            if (sig < nsig) {
+            if (ARGMAX && sig < nsig) {
                 *reinterpret_cast<int4*>(bk + j0) = make_int4(arg[x][0], arg[x][1], arg[x][2], arg[x][3]);
                 *reinterpret_cast<int4*>(bk + j1) = make_int4(arg[x][4], arg[x][5], arg[x][6], arg[x][7]);
+            }
+            if (!ARGMAX && sig < nsig && t + 1 < T) {      // chi_t, read back by the backtrack
+                double* h = hist + (sig * steps + t) * (int64_t)S;
+                *reinterpret_cast<double2*>(h + j0) = make_double2(best[x][0], best[x][1]);
+                *reinterpret_cast<double2*>(h + j0 + 2) = make_double2(best[x][2], best[x][3]);
+                *reinterpret_cast<double2*>(h + j1) = make_double2(best[x][4], best[x][5]);
+                *reinterpret_cast<double2*>(h + j1 + 2) = make_double2(best[x][6], best[x][7]);
             }
         }
 #pragma unroll
@@ -185,26 +207,107 @@ __global__ void k_viterbi_backtrack(const double* __restrict__ chi, const int* _
     logp[sig] = c[bi];
 }
 
+// Recomputing backtrack: s_{t-1} = first argmax_i (chi_{t-1}[i] + logA[i][s_t])
+// with logA^T rows contiguous (lAT[j][i]); one warp per signal.
+__global__ void k_viterbi_backtrack_recompute(const double* __restrict__ chi, const double* __restrict__ hist,
+                                              const double* __restrict__ lAT, int S, int64_t nsig, int T,
+                                              int* __restrict__ path, double* __restrict__ logp) {
+    const int64_t sig = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (sig >= nsig) return;
+    auto warp_argmax = [&](double bv, int bi) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        return bi == 0x7fffffff ? 0 : bi;
+    };
+    const double* c = chi + sig * S;
+    double bv = __longlong_as_double(0xfff0000000000000ll);
+    int bi = 0x7fffffff;
+    for (int i = lane; i < S; i += 32) {
+        const double v = c[i];
+        if (v > bv) { bv = v; bi = i; }        // lanes scan increasing i: strict > keeps the first
+    }
+    int s = warp_argmax(bv, bi);
+    const int64_t steps = T > 1 ? T - 1 : 0;
+    int* p = path + sig * T;
+    if (lane == 0) { p[T - 1] = s; logp[sig] = c[s]; }
+    for (int t = T - 1; t >= 1; --t) {
+        const double* h = hist + (sig * steps + (t - 1)) * (int64_t)S;
+        const double* col = lAT + (int64_t)s * S;
+        bv = __longlong_as_double(0xfff0000000000000ll);
+        bi = 0x7fffffff;
+#pragma unroll 4
+        for (int i = lane; i < S; i += 32) {
+            const double v = __dadd_rn(h[i], col[i]);
+            if (v > bv) { bv = v; bi = i; }
+        }
+        s = warp_argmax(bv, bi);
+        if (lane == 0) p[t - 1] = s;
+    }
+}
+
+__global__ void k_transpose_f64(const double* __restrict__ a, double* __restrict__ at, int S) {
+    __shared__ double tile[32][33];
+    const int bi = blockIdx.y * 32, bj = blockIdx.x * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) tile[r][threadIdx.x] = a[(int64_t)(bi + r) * S + bj + threadIdx.x];
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) at[(int64_t)(bj + r) * S + bi + threadIdx.x] = tile[threadIdx.x][r];
+}
+
 bool viterbi_tiled_eligible(int S) { return S == 256 || S == 512 || S == 1024; }
 
+// workspace of the tiled path: max(back pointers int32, chi history fp64) | final chi | log A^T
+size_t viterbi_tiled_workspace(int S, int64_t nsig, int T) {
+    const size_t steps = (size_t)(T > 1 ? T - 1 : 0);
+    const size_t h = ((size_t)nsig * steps * (size_t)S * sizeof(double) + 255) & ~(size_t)255;
+    const size_t c = ((size_t)nsig * (size_t)S * sizeof(double) + 255) & ~(size_t)255;
+    return h + c + (size_t)S * S * sizeof(double) + 256;
+}
+
 int viterbi_tiled_launch(const double* log_pi, const double* log_A, const double* log_E, int S, int K,
-                         const int* obs, int64_t nsig, int T, int* path, double* logp, int* back,
-                         double* chi_final, cudaStream_t st) {
-#define PMX_VT(SS)                                                                                 \
+                         const int* obs, int64_t nsig, int T, int* path, double* logp, void* ws,
+                         cudaStream_t st) {
+    // Default: argmax kept in the forward (back pointers). PMX_VITERBI_RECOMPUTE=1:
+    // scores only + recomputing backtrack — measured slower (476 vs 353 ms at
+    // the bench config): sm_100 has no fp64 max instruction, fmax lowers to
+    // DSETP + selects, so a cell costs the same issue slots either way.
+    static const bool argmax = !(getenv("PMX_VITERBI_RECOMPUTE") && getenv("PMX_VITERBI_RECOMPUTE")[0] == '1');
+    const size_t steps = (size_t)(T > 1 ? T - 1 : 0);
+    const size_t h = ((size_t)nsig * steps * (size_t)S * sizeof(double) + 255) & ~(size_t)255;
+    const size_t c = ((size_t)nsig * (size_t)S * sizeof(double) + 255) & ~(size_t)255;
+    int* back = (int*)ws;
+    double* hist = (double*)ws;
+    double* chi_final = (double*)((char*)ws + h);
+    double* lAT = (double*)((char*)ws + h + c);
+#define PMX_VT(SS, AM)                                                                             \
     if (S == SS) {                                                                                 \
         constexpr int MS = 4 * (VT_NT / (SS / 8));                                                 \
         const size_t smem = ((size_t)SS * MS + 2 * (size_t)VT_KT * SS) * sizeof(double);           \
-        cudaFuncSetAttribute(k_viterbi_tiled<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+        cudaFuncSetAttribute(k_viterbi_tiled<SS, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              (int)smem);                                                           \
-        k_viterbi_tiled<SS><<<(unsigned)((nsig + MS - 1) / MS), VT_NT, smem, st>>>(                \
-            log_pi, log_A, log_E, K, obs, nsig, T, back, chi_final);                               \
+        k_viterbi_tiled<SS, AM><<<(unsigned)((nsig + MS - 1) / MS), VT_NT, smem, st>>>(            \
+            log_pi, log_A, log_E, K, obs, nsig, T, back, hist, chi_final);                         \
         PMX_CHECK_LAUNCH("viterbi_tiled");                                                         \
     }
-    PMX_VT(1024)
-    PMX_VT(512)
-    PMX_VT(256)
+    if (argmax) {
+        PMX_VT(1024, true)
+        PMX_VT(512, true)
+        PMX_VT(256, true)
+        k_viterbi_backtrack<<<(unsigned)((nsig + 7) / 8), 256, 0, st>>>(chi_final, back, S, nsig, T, path, logp);
+        PMX_CHECK_LAUNCH("viterbi_backtrack");
+        return 0;
+    }
+    PMX_VT(1024, false)
+    PMX_VT(512, false)
+    PMX_VT(256, false)
 #undef PMX_VT
-    k_viterbi_backtrack<<<(unsigned)((nsig + 7) / 8), 256, 0, st>>>(chi_final, back, S, nsig, T, path, logp);
+    k_transpose_f64<<<dim3(S / 32, S / 32), dim3(32, 8), 0, st>>>(log_A, lAT, S);
+    PMX_CHECK_LAUNCH("viterbi_transpose");
+    k_viterbi_backtrack_recompute<<<(unsigned)((nsig + 7) / 8), 256, 0, st>>>(chi_final, hist, lAT, S, nsig, T,
+                                                                             path, logp);
     PMX_CHECK_LAUNCH("viterbi_backtrack");
     return 0;
 }

@@ -567,6 +567,67 @@ def cpu_viterbi(seconds=10.0) -> dict:
             "cores": th, "kind": "port", "sample": f"{reps}x {obs.shape[0]} signals x {T} steps at S=1024"}
 
 
+def bench_nn(args, dist, peaks) -> dict:
+    """Softmax-regression loss + gradients (programs/nn.pmx) at scale: SURVEY
+    §8(f) rank 3.  2^20 points, 64 inputs, 16 classes, fp64 (the reference's
+    Float); x is the only HBM stream (512 MiB)."""
+    import numpy as np
+    import torch
+    from paper_2211_00621_b200 import _lib
+    npts, nin, nout = 1 << 20, 64, 16
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev).manual_seed(3)
+    x = torch.randn(npts * nin, dtype=torch.float64, device=dev, generator=g) * 0.5
+    y = torch.randint(0, nout, (npts,), dtype=torch.int32, device=dev, generator=g)
+    w = torch.randn(nin * nout, dtype=torch.float64, device=dev, generator=g) * 0.3
+    b = torch.randn(nout, dtype=torch.float64, device=dev, generator=g) * 0.1
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    dw = torch.empty(nin * nout, dtype=torch.float64, device=dev)
+    db = torch.empty(nout, dtype=torch.float64, device=dev)
+    err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    ws = torch.zeros(lib.pmx_nn_workspace_bytes(npts, nin, nout), dtype=torch.uint8, device=dev)
+
+    def step():
+        _lib.check(lib.pmx_nn_softmax_grad_f64(x.data_ptr(), y.data_ptr(), w.data_ptr(), b.data_ptr(), npts, nin,
+                                               nout, loss.data_ptr(), dw.data_ptr(), db.data_ptr(), ws.data_ptr(),
+                                               ws.numel(), err.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                   "nn")
+    total, per = device_time(step, args.steps, args.warmup, dist)
+    ms = total / args.steps
+    bytes_ = 8.0 * nin * npts + 4.0 * npts
+    flops = npts * (2.0 * nin * nout * 2)            # z (mul+add) and dw (mul+add), fp64
+    return {"config": f"{npts} points x {nin} inputs x {nout} classes, fp64 (nn.pmx semantics)", "element": "point",
+            "value": npts * dist.world / (ms * 1e-3), "ms_per_step": ms,
+            "roofline": {"bound": "HBM (x stream) / FP64 pipe", "achieved_GBps": bytes_ / (ms * 1e-3) / 1e9,
+                         "hbm_frac": bytes_ / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "achieved_fp64_tflops": flops / (ms * 1e-3) / 1e12,
+                         "fp64_frac": flops / (ms * 1e-3) / 1e12 / 37.0,
+                         "peak_source": "HBM measured; FP64 37 TFLOP/s (64 lanes x 2 x 148 SMs x 1.965 GHz)"},
+            "_loss": float(loss.item())}
+
+
+def cpu_nn(seconds=10.0) -> dict:
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import numpy as np
+    import oracle as O
+    n, nin, nout = 1 << 16, 64, 16
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((n, nin))
+    y = rng.integers(0, nout, n).astype(np.int32)
+    w = rng.standard_normal((nin, nout))
+    b = rng.standard_normal(nout)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        O.nn(x, y, w, b, workers=1)
+        reps += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": n / dt, "unit": "points/s", "cores": 1, "kind": "port",
+            "sample": f"{reps}x 2^16 of the 2^20 points (oracle_nn is single-threaded)"}
+
+
 def bench_kmer(args, dist, peaks) -> dict:
     import numpy as np
     import torch
@@ -631,7 +692,7 @@ def run_ours(args):
     if not args.no_case_studies:
         for name, fn, cfn in (("rk4", bench_rk4, cpu_rk4), ("knn", bench_knn, cpu_knn),
                               ("hmm_forward", bench_hmm, cpu_hmm), ("hmm_kmer", bench_kmer, cpu_kmer),
-                              ("viterbi", bench_viterbi, cpu_viterbi)):
+                              ("viterbi", bench_viterbi, cpu_viterbi), ("nn", bench_nn, cpu_nn)):
             if args.case and name not in args.case:
                 continue
             try:

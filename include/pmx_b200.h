@@ -286,6 +286,18 @@ PMX_API int pmx_viterbi_f64(const double* log_pi, const double* log_A,
                     int32_t* path, double* logp, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* Softmax regression (programs/nn.pmx:22-49): mean cross-entropy loss and its
+ * analytic gradients for npts points, one fused launch.  x [npts*nin] fp64,
+ * y [npts] int32 class labels, w [nin*nout], b [nout]; outputs loss [1],
+ * dw [nin*nout], db [nout] (device pointers).  nin <= 64, nout <= 32.
+ * Runtime errors (class label out of range, exp overflow, npts == 0 ->
+ * "float division by zero" as divf _ 0.0) go to the error word.            */
+PMX_API size_t pmx_nn_workspace_bytes(int64_t npts, int32_t nin, int32_t nout);
+PMX_API int pmx_nn_softmax_grad_f64(const double* x, const int32_t* y, const double* w, const double* b,
+                            int64_t npts, int32_t nin, int32_t nout, double* loss, double* dw,
+                            double* db, void* workspace, size_t workspace_bytes, uint64_t* err,
+                            void* stream);
+
 /* k-NN classification: label of each query = majority
  * vote of the k nearest train points by squared L2 distance, ties by smaller
  * train index, vote ties to the smaller label.  train [ntr*d] f32, query

@@ -45,6 +45,8 @@ def lib():
         L.oracle_knn.argtypes = [P, P, C.c_int64, P, C.c_int64, C.c_int, C.c_int, C.c_int, P, P, C.c_int]
         L.oracle_kmer_forward.argtypes = [C.c_int, C.c_double, C.c_double, P, C.c_int, P, C.c_int64,
                                           C.c_int, P, C.c_int]
+        L.oracle_nn.restype = C.c_int64
+        L.oracle_nn.argtypes = [P, P, P, P, C.c_int64, C.c_int, C.c_int, C.c_int64, P, P, P]
         L.oracle_max_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -269,3 +271,22 @@ def ir_reduce(f, acc, xs, workers: int = 1):   # eval_reduce, interp.py:328-343
     for p in parts[1:]:
         total = ir_apply(f, total, p)
     return total
+
+
+def nn(x, y, w, b, workers: int = 4):
+    """(loss, dw, db) of programs/nn.pmx:22-49 with the reference's chunked
+    top-level reduces over `workers` chunks.  Raises ValueError on a label out
+    of range (the reference's get error)."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.int32)
+    w = np.ascontiguousarray(w, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    npts, nin = x.shape
+    nout = b.size
+    loss = np.zeros(1, np.float64)
+    dw = np.empty((nin, nout), np.float64)
+    db = np.empty(nout, np.float64)
+    bad = lib().oracle_nn(_p(x), _p(y), _p(w), _p(b), npts, nin, nout, workers, _p(loss), _p(dw), _p(db))
+    if bad:
+        raise ValueError(f"label out of range at point {bad - 1}")
+    return float(loss[0]), dw, db

@@ -5,7 +5,7 @@ Operator surface (same names and meaning as pmx/interp.py's hot path):
     accelerate / device_call, eval_map, eval_map2, eval_reduce, fold (foldl),
     eval_loop, seq_loop, flatten, marshal_in / marshal_out, merge_intervals,
     Heap, TensorView, Diagnostics
-Case studies: rk4_sweep, hmm_forward, viterbi, knn_classify, hmm_kmer_forward.
+Case studies: rk4_sweep, hmm_forward, viterbi, knn_classify, hmm_kmer_forward, nn_gradients.
 
 All computation runs in libpmxb200.so (hand-written sm_100a CUDA behind a C
 ABI, include/pmx_b200.h); PyTorch supplies device memory and streams only.
@@ -29,7 +29,7 @@ from .skeletons import (
     PREV, Ctx, LazyMap, accelerate, device_call, eval_loop, eval_map, eval_map2, eval_reduce, flatten,
     fold, seq_loop,
 )
-from .casestudies import hmm_forward, hmm_kmer_forward, knn_classify, rk4_sweep, viterbi
+from .casestudies import hmm_forward, hmm_kmer_forward, knn_classify, nn_gradients, rk4_sweep, viterbi
 
 __all__ = [n for n in dir() if not n.startswith("_")]
 

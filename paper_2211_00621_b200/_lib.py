@@ -108,6 +108,9 @@ _SIGS = {
     "pmx_viterbi_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int64, C.c_int32]),
     "pmx_viterbi_f64": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, _P, C.c_int64, C.c_int32,
                                   _P, _P, _P, C.c_size_t, _P]),
+    "pmx_nn_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32]),
+    "pmx_nn_softmax_grad_f64": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P,
+                                          C.c_size_t, _P, _P]),
     "pmx_knn_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int64, C.c_int32, C.c_int32]),
     "pmx_knn_f32": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                               _P, _P, _P, C.c_size_t, _P]),

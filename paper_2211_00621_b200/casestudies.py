@@ -11,6 +11,7 @@ values (host values when called outside accelerate through `accelerate`).
     viterbi           programs/viterbi.pmx:23-59          (viterbi trans emit init obs)
     knn_classify      SURVEY Appendix A.2 knn.pmx          (classify train labels queries)
     hmm_kmer_forward  SURVEY §8(d) nanopore k-mer model
+    nn_gradients      programs/nn.pmx:22-49               (gradients xs ys w b)
 """
 from __future__ import annotations
 
@@ -197,3 +198,35 @@ def hmm_kmer_forward(kmer: int, p_stay: float, p_step: float, emit, obs) -> Devi
     _lib.check(rc, "hmm_kmer_forward")
     _count()
     return DeviceSeq(out, (nsig,), _lib.PMX_F64)
+
+
+# ------------------------------------------------------------- NN gradients
+def nn_gradients(xs, ys, w, b):
+    """{loss, dw, db} of softmax regression (programs/nn.pmx:22-49): mean
+    cross-entropy over the points and its analytic gradients, fp64, one fused
+    launch.  xs [npts][nin], ys [npts] class labels, w [nin][nout], b [nout]."""
+    from .runtime import DeviceScalar
+    from .diagnostics import NO_SPAN
+    X = _dev(xs, torch.float64)
+    Y = _dev(ys, torch.int32)
+    W = _dev(w, torch.float64)
+    B = _dev(b, torch.float64)
+    nout = B.numel()
+    nin = W.numel() // max(nout, 1)
+    npts = Y.numel()
+    if X.numel() != npts * nin:
+        raise runtime_error(f"nn_gradients: xs has {X.numel()} values, expected {npts} x {nin}")
+    loss = torch.empty(1, dtype=torch.float64, device=_device())
+    dw = torch.empty(nin * nout, dtype=torch.float64, device=_device())
+    db = torch.empty(nout, dtype=torch.float64, device=_device())
+    lib = _lib.load()
+    ws = _ws.get(lib.pmx_nn_workspace_bytes(npts, nin, nout))
+    err = default_ctx().new_err(NO_SPAN)
+    rc = lib.pmx_nn_softmax_grad_f64(X.data_ptr(), Y.data_ptr(), W.data_ptr(), B.data_ptr(), npts, nin, nout,
+                                     loss.data_ptr(), dw.data_ptr(), db.data_ptr(), ws.data_ptr(), ws.numel(),
+                                     err.data_ptr(), _stream())
+    _lib.check(rc, "nn_gradients")
+    _count()
+    return {"loss": DeviceScalar(loss, True, err, NO_SPAN),
+            "dw": DeviceSeq(dw, (nin, nout), _lib.PMX_F64),
+            "db": DeviceSeq(db, (nout,), _lib.PMX_F64)}

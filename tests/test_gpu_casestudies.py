@@ -183,3 +183,74 @@ def test_kmer_vs_oracle(kmer, nsig, T):
     got = accelerate(lambda em, o: hmm_kmer_forward(kmer, 0.5, 0.125, em, o), E, obs)
     want = O.kmer_forward(kmer, 0.5, 0.125, E, obs)
     assert np.allclose(got, want, rtol=LL_REL, atol=0)
+
+
+# ---------------------------------------------------------- NN gradients
+def _nn_ref_data():
+    n_in, n_out, n_pts = 16, 8, 32
+    x = np.array([[((p * 5 + i * 3) % 11 - 5) / 10.0 for i in range(n_in)] for p in range(n_pts)])
+    y = np.array([(p * 7 + 3) % n_out for p in range(n_pts)], np.int32)
+    w = np.array([[((i * 3 + j * 7) % 13 - 6) / 20.0 for j in range(n_out)] for i in range(n_in)])
+    b = np.array([((j * 5) % 9 - 4) / 15.0 for j in range(n_out)])
+    return x, y, w, b
+
+
+def _nn_loss(x, y, w, b):
+    z = x @ w + b
+    return float(np.mean(np.log(np.sum(np.exp(z), axis=1)) - z[np.arange(len(y)), y]))
+
+
+def test_nn_reference_program(golden):
+    # programs/nn.pmx: loss, dw, db against the reference's printed values
+    # (sums over points in a different order than its 4 workers: rel 1e-12)
+    from paper_2211_00621_b200 import nn_gradients
+    r = accelerate(nn_gradients, *_nn_ref_data())
+    lines = [l for l in golden["program_nn"]["stdout"].splitlines() if l.strip()]
+    assert math.isclose(r["loss"], float(lines[0]), rel_tol=1e-12)
+    want_dw = np.array([[float(v) for v in l.split()] for l in lines[1:17]])
+    want_db = np.array([float(v) for v in lines[17].split()])
+    assert np.allclose(np.asarray(r["dw"]).reshape(16, 8), want_dw, rtol=1e-12, atol=1e-17)
+    assert np.allclose(np.asarray(r["db"]), want_db, rtol=1e-12, atol=1e-17)
+
+
+def test_nn_gradients_match_finite_differences():
+    # the reference's own check (tests/test_acceptance.py:424-441)
+    from paper_2211_00621_b200 import nn_gradients
+    x, y, w, b = _nn_ref_data()
+    r = accelerate(nn_gradients, x, y, w, b)
+    dw = np.asarray(r["dw"]).reshape(16, 8)
+    eps = 1e-5
+    for i in range(16):
+        for j in range(8):
+            wp, wm = w.copy(), w.copy()
+            wp[i, j] += eps
+            wm[i, j] -= eps
+            fd = (_nn_loss(x, y, wp, b) - _nn_loss(x, y, wm, b)) / (2 * eps)
+            assert math.isclose(dw[i, j], fd, rel_tol=1e-4, abs_tol=1e-8)
+
+
+@pytest.mark.parametrize("npts,nin,nout", [(100_003, 64, 16), (4097, 7, 32), (1, 3, 1), (50_000, 33, 5)])
+def test_nn_vs_oracle(npts, nin, nout):
+    from paper_2211_00621_b200 import nn_gradients
+    rng = np.random.default_rng(npts + nin)
+    x = rng.standard_normal((npts, nin)) * 0.5
+    y = rng.integers(0, nout, npts).astype(np.int32)
+    w = rng.standard_normal((nin, nout)) * 0.3
+    b = rng.standard_normal(nout) * 0.1
+    r = accelerate(nn_gradients, x, y, w, b)
+    loss, dw, db = O.nn(x, y, w, b, workers=4)
+    assert math.isclose(r["loss"], loss, rel_tol=1e-11)
+    assert np.allclose(np.asarray(r["dw"]).reshape(nin, nout), dw, rtol=1e-9, atol=1e-14)
+    assert np.allclose(np.asarray(r["db"]), db, rtol=1e-9, atol=1e-14)
+
+
+def test_nn_errors():
+    from paper_2211_00621_b200 import Diagnostics, nn_gradients
+    x, y, w, b = _nn_ref_data()
+    y = y.copy()
+    y[9] = 8
+    with pytest.raises(Diagnostics, match="out of bounds") as ei:
+        accelerate(nn_gradients, x, y, w, b)
+    assert "element 9)" in str(ei.value)
+    with pytest.raises(Diagnostics, match="float division by zero"):
+        accelerate(nn_gradients, np.zeros((0, 16)), np.zeros(0, np.int32), w, b)

@@ -157,3 +157,31 @@ def test_chunks_rule():
         O.lib().oracle_chunk(10, 4, i, C.byref(lo), C.byref(hi))
         spans.append((lo.value, hi.value))
     assert spans == [(0, 2), (2, 5), (5, 7), (7, 10)]
+
+
+def _nn_data():
+    # programs/nn.pmx:5-21 (= tests/test_acceptance.py:399-410 of the reference)
+    n_in, n_out, n_pts = 16, 8, 32
+    x = np.array([[((p * 5 + i * 3) % 11 - 5) / 10.0 for i in range(n_in)] for p in range(n_pts)])
+    y = np.array([(p * 7 + 3) % n_out for p in range(n_pts)], np.int32)
+    w = np.array([[((i * 3 + j * 7) % 13 - 6) / 20.0 for j in range(n_out)] for i in range(n_in)])
+    b = np.array([((j * 5) % 9 - 4) / 15.0 for j in range(n_out)])
+    return x, y, w, b
+
+
+def test_nn_oracle_matches_reference_program(golden):
+    # the reference ran programs/nn.pmx in accel mode with 4 workers: same
+    # chunked reduces, same libm -> bit-identical printed values
+    lines = [l for l in golden["program_nn"]["stdout"].splitlines() if l.strip()]
+    loss, dw, db = O.nn(*_nn_data(), workers=4)
+    assert loss == float(lines[0])
+    assert [[float(v) for v in l.split()] for l in lines[1:17]] == dw.tolist()
+    assert [float(v) for v in lines[17].split()] == db.tolist()
+
+
+def test_nn_oracle_label_out_of_range():
+    x, y, w, b = _nn_data()
+    y = y.copy()
+    y[5] = 8
+    with pytest.raises(ValueError, match="point 5"):
+        O.nn(x, y, w, b)

@@ -265,6 +265,13 @@ PMX_API int pmx_map_reduce_peers(const pmx_program* f, const pmx_program* op,
 PMX_API int pmx_rk4_sweep_f64(const double* params, int64_t n, const double* init4,
                       int32_t steps, double h, double* out, void* stream);
 
+/* The paper's ODE study output: the same sweep, also
+ * recording state component `comp` (0..3) after every step into the N x M
+ * tensor trace[k * steps + m] (row-major, device pointer: a tensor view's
+ * root + offset).  out[k*4 + c] receives the final states.                   */
+PMX_API int pmx_rk4_trace_f64(const double* params, int64_t n, const double* init4, int32_t steps,
+                      double h, int32_t comp, double* trace, double* out, void* stream);
+
 /* Log-space HMM forward for nsig signals of length T:
  * out_ll[s] = log P(obs[s, 0:T]).  log_pi[S], A[S*S] row-major probabilities
  * (A[i*S+j] = P(j | i)), log_E[S*K] (log_E[j*K+k]), obs int32 [nsig*T].

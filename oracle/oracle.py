@@ -40,6 +40,7 @@ def lib():
         L.oracle_map_affine_reduce_add.argtypes = [P, C.c_int64, C.c_double, C.c_double, C.c_double,
                                                    C.c_int64, C.c_int, P]
         L.oracle_rk4.argtypes = [P, C.c_int64, P, C.c_int, C.c_double, P, C.c_int]
+        L.oracle_rk4_trace.argtypes = [P, C.c_int64, P, C.c_int, C.c_double, P, C.c_int, P, C.c_int]
         L.oracle_hmm_forward.argtypes = [P, P, P, C.c_int, C.c_int, P, C.c_int64, C.c_int, P, C.c_int]
         L.oracle_viterbi.argtypes = [P, P, P, C.c_int, C.c_int, P, C.c_int64, C.c_int, P, P, C.c_int]
         L.oracle_knn.argtypes = [P, P, C.c_int64, P, C.c_int64, C.c_int, C.c_int, C.c_int, P, P, C.c_int]
@@ -75,6 +76,16 @@ def rk4(params: np.ndarray, init4, steps: int, h: float, threads: int | None = N
     out = np.empty((p.size, 4), np.float64)
     lib().oracle_rk4(_p(p), p.size, _p(s0), steps, h, _p(out), threads or threads_default())
     return out
+
+
+def rk4_trace(params, init4, steps: int, h: float, comp: int, threads: int | None = None):
+    """(final states [N][4], trace [N][steps] of state `comp`) — PAPER.md:1435-1440."""
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    s0 = np.ascontiguousarray(init4, dtype=np.float64)
+    out = np.empty((p.size, 4), np.float64)
+    tr = np.empty((p.size, steps), np.float64)
+    lib().oracle_rk4_trace(_p(p), p.size, _p(s0), steps, h, _p(out), comp, _p(tr), threads or threads_default())
+    return out, tr
 
 
 def hmm_forward(A, E, pi, obs, threads: int | None = None) -> np.ndarray:

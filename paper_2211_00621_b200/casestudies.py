@@ -75,6 +75,37 @@ def rk4_sweep(params, init4, steps: int, h: float) -> DeviceSeq:
     return DeviceSeq(out, (n, 4), _lib.PMX_F64)
 
 
+def rk4_trace(params, init4, steps: int, h: float, comp: int = 2, trace=None):
+    """The paper's ODE study: N simulation traces of one
+    measured state component, an N x M tensor with trace[k][m] = component
+    `comp` of integrate p_k after m + 1 steps.  `trace` may be a tensor view
+    marshalled into the accelerated region (written in place in its device
+    root, like the paper's `loop ... tensorSet`); otherwise a new N x M
+    sequence is returned.  Returns (trace, final states)."""
+    from .runtime import DeviceTensor
+    p = _dev(params, torch.float64)
+    s0 = _dev(init4, torch.float64)
+    if s0.numel() != 4:
+        raise runtime_error("rk4: the state has 4 components")
+    n = p.numel()
+    out = torch.empty(n * 4, dtype=torch.float64, device=_device())
+    if isinstance(trace, DeviceTensor):
+        if tuple(trace.shape) != (n, int(steps)) or trace.root.dtype_code != _lib.PMX_F64:
+            raise runtime_error(f"rk4_trace: trace tensor must be [{n}][{steps}] Float, got {list(trace.shape)}")
+        ptr = trace.root.data.data_ptr() + 8 * trace.offset
+        trace.root.dirty = True           # written root: copied back by marshal_out
+        res = trace
+    else:
+        buf = torch.empty(n * int(steps), dtype=torch.float64, device=_device())
+        ptr = buf.data_ptr()
+        res = DeviceSeq(buf, (n, int(steps)), _lib.PMX_F64)
+    rc = _lib.load().pmx_rk4_trace_f64(p.data_ptr(), n, s0.data_ptr(), int(steps), float(h), int(comp), ptr,
+                                       out.data_ptr(), _stream())
+    _lib.check(rc, "rk4_trace")
+    _count()
+    return res, DeviceSeq(out, (n, 4), _lib.PMX_F64)
+
+
 # ------------------------------------------------------------------ HMM
 class HMMWorkspace:
     def __init__(self):

@@ -48,9 +48,13 @@ __device__ __forceinline__ double comb(double s, double h6, double k1, double k2
     return A_(s, M_(h6, A_(k1, A_(M_(2.0, k2), A_(M_(2.0, k3), k4)))));
 }
 
+// TRACE: also record state component `comp` after every step into
+// trace[k * steps + m] (the paper's N x M tensor of one measured state,
+// PAPER.md:1435-1440, written by its accelerated `loop` through tensorSet).
+template <bool TRACE>
 __global__ void __launch_bounds__(64)
 k_rk4(const double* __restrict__ ps, int64_t n, const double* __restrict__ init4,
-      int steps, double h, double* __restrict__ out) {
+      int steps, double h, double* __restrict__ out, int comp, double* __restrict__ trace) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double p = ps[k];
@@ -64,6 +68,10 @@ k_rk4(const double* __restrict__ ps, int64_t n, const double* __restrict__ init4
         const St k4 = deriv(p, axpy(s, h, k3));
         s = St{comb(s.x0, h6, k1.x0, k2.x0, k3.x0, k4.x0), comb(s.x1, h6, k1.x1, k2.x1, k3.x1, k4.x1),
                comb(s.x2, h6, k1.x2, k2.x2, k3.x2, k4.x2), comb(s.x3, h6, k1.x3, k2.x3, k3.x3, k4.x3)};
+        if (TRACE) {
+            const double v = comp == 0 ? s.x0 : comp == 1 ? s.x1 : comp == 2 ? s.x2 : s.x3;
+            __stcs(trace + k * (int64_t)steps + m, v);
+        }
     }
     double* o = out + 4 * k;
     o[0] = s.x0; o[1] = s.x1; o[2] = s.x2; o[3] = s.x3;
@@ -81,7 +89,20 @@ extern "C" int pmx_rk4_sweep_f64(const double* params, int64_t n, const double* 
     // 64 threads per CTA spreads the few warps of an N=10^4 sweep over all SMs.
     const int threads = 64;
     const int64_t grid = (n + threads - 1) / threads;
-    k_rk4<<<(unsigned)grid, threads, 0, (cudaStream_t)stream>>>(params, n, init4, steps, h, out);
+    k_rk4<false><<<(unsigned)grid, threads, 0, (cudaStream_t)stream>>>(params, n, init4, steps, h, out, 0, nullptr);
     PMX_CHECK_LAUNCH("rk4");
+    return 0;
+}
+
+extern "C" int pmx_rk4_trace_f64(const double* params, int64_t n, const double* init4, int32_t steps, double h,
+                                 int32_t comp, double* trace, double* out, void* stream) {
+    PMX_REQUIRE(n >= 0 && steps >= 0, "pmx_rk4_trace_f64: negative size");
+    PMX_REQUIRE(comp >= 0 && comp < 4, "pmx_rk4_trace_f64: state component must be 0..3");
+    if (n == 0) return 0;
+    PMX_REQUIRE(params && init4 && out && (trace || steps == 0), "pmx_rk4_trace_f64: null buffer");
+    const int threads = 64;
+    const int64_t grid = (n + threads - 1) / threads;
+    k_rk4<true><<<(unsigned)grid, threads, 0, (cudaStream_t)stream>>>(params, n, init4, steps, h, out, comp, trace);
+    PMX_CHECK_LAUNCH("rk4_trace");
     return 0;
 }

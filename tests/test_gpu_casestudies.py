@@ -254,3 +254,33 @@ def test_nn_errors():
     assert "element 9)" in str(ei.value)
     with pytest.raises(Diagnostics, match="float division by zero"):
         accelerate(nn_gradients, np.zeros((0, 16)), np.zeros(0, np.int32), w, b)
+
+
+# ------------------------------------------------------------ RK4 trace
+def test_rk4_trace_vs_oracle():
+    # the paper's N x M trace of one measured state
+    from paper_2211_00621_b200 import rk4_trace
+    ps = synth.rk4_params(300)
+    tr, fin = accelerate(lambda p, s: rk4_trace(p, s, 200, synth.RK4_H, 2), ps, synth.RK4_INIT)
+    want_fin, want_tr = O.rk4_trace(ps, synth.RK4_INIT, 200, synth.RK4_H, 2)
+    assert np.asarray(tr).shape == (300, 200)
+    assert np.allclose(np.asarray(tr), want_tr, rtol=1e-9, atol=1e-12)
+    assert np.allclose(np.asarray(fin), want_fin, rtol=1e-9, atol=1e-12)
+    assert np.array_equal(np.asarray(tr)[:, -1], np.asarray(fin)[:, 2])
+
+
+def test_rk4_trace_into_aliased_tensor_view():
+    # trace written through a tensor view of a larger heap buffer (tensorSub,
+    # Alg. 2 root): only the view's rows change, the rest of the buffer stays
+    from paper_2211_00621_b200 import Ctx, Heap, TensorView, rk4_trace
+    n, m = 50, 30
+    heap = Heap()
+    buf = heap.alloc(np.full((n + 4) * m, -7.0))
+    view = TensorView(buf, 2 * m, (n, m), "float")          # rows 2 .. n+1
+    ps = synth.rk4_params(n)
+    accelerate(lambda p, s, t: rk4_trace(p, s, m, synth.RK4_H, 0, trace=t)[1], ps, synth.RK4_INIT, view,
+               ctx=Ctx(heap=heap))
+    got = heap.buffers[buf].reshape(n + 4, m)
+    _, want = O.rk4_trace(ps, synth.RK4_INIT, m, synth.RK4_H, 0)
+    assert np.allclose(got[2:n + 2], want, rtol=1e-9, atol=1e-12)
+    assert (got[:2] == -7.0).all() and (got[n + 2:] == -7.0).all()

@@ -420,4 +420,48 @@ k_loop_lanes(int64_t n, const B body, uint64_t* err) {
     }
 }
 
+// ---- elementwise parallel loop (tensor accesses at [i] only) ----------------
+// Packets of 4 consecutive iterations with vector loads/stores (B::vec), VP
+// packets per thread interleaved statement by statement; the < 4 tail
+// iterations run through the bounds-checked lane path.
+template <class B, int VP>
+__global__ void __launch_bounds__(256, 4)
+k_loop_vec(int64_t n, const B body, uint64_t* err) {
+    const int64_t npk = n / 4;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; p + (VP - 1) * gs < npk; p += VP * gs) {
+        int64_t pk[VP];
+        int code[4 * VP];
+#pragma unroll
+        for (int q = 0; q < VP; ++q) pk[q] = p + q * gs;
+#pragma unroll
+        for (int u = 0; u < 4 * VP; ++u) code[u] = 0;
+        body.template vec<VP>(pk, code);
+#pragma unroll
+        for (int u = 0; u < 4 * VP; ++u)
+            if (code[u]) raise_err(err, 4 * pk[u >> 2] + (u & 3), code[u]);
+    }
+    for (; p < npk; p += gs) {
+        int64_t pk[1] = {p};
+        int code[4] = {0, 0, 0, 0};
+        body.template vec<1>(pk, code);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (code[u]) raise_err(err, 4 * p + u, code[u]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 4) {
+        const int64_t i0 = 4 * npk + threadIdx.x;
+        int64_t i[B::U];
+        int code[B::U];
+#pragma unroll
+        for (int u = 0; u < B::U; ++u) {
+            i[u] = i0;
+            code[u] = (u == 0 && i0 < n) ? 0 : -1;
+        }
+        body(i, code);
+        if (code[0] > 0) raise_err(err, i0, code[0]);
+    }
+}
+
 }  // namespace pmx

@@ -144,3 +144,60 @@ def test_gather_from_captured_sequence():
     with pytest.raises(P.Diagnostics, match="out of bounds") as ei:
         P.accelerate(lambda d, s: P.eval_map(P.lam("i", P.get(d, "i")), s), data, bad)
     assert "element 123456)" in str(ei.value)
+
+
+def _tensor(t, bid):
+    return DeviceTensor(_Root(t, bid, 0, t.numel(), {torch.float32: _lib.PMX_F32, torch.float64: _lib.PMX_F64,
+                                                      torch.int64: _lib.PMX_I64}[t.dtype]), 0, (t.numel(),), "float")
+
+
+def test_elementwise_loop_inplace_and_types():
+    # vectorised elementwise loop: in-place update, f64 and i64 views, ragged n
+    n = N
+    dev = torch.device("cuda", 0)
+    y = torch.arange(n, dtype=torch.float64, device=dev) * 0.5
+    ty = _tensor(y, 0)
+    before = _launched()
+    P.eval_loop(n, P.lam("i", P.tensor_set(ty, ["i"], P.subf(P.mulf(P.tensor_get(ty, ["i"]), 3.0), 1.0))))
+    default_ctx().check_errors()
+    assert _launched() > before
+    ref = np.arange(n, dtype=np.float64) * 0.5 * 3.0 - 1.0
+    assert np.array_equal(y.cpu().numpy(), ref)
+    z = torch.zeros(n, dtype=torch.int64, device=dev)
+    tz = DeviceTensor(_Root(z, 1, 0, n, _lib.PMX_I64), 0, (n,), "int")
+    P.eval_loop(n, P.lam("i", P.tensor_set(tz, ["i"], P.addi(P.muli("i", "i"), P.modi("i", 7)))))
+    default_ctx().check_errors()
+    i = np.arange(n, dtype=np.int64)
+    assert np.array_equal(z.cpu().numpy(), i * i + i % 7)
+
+
+def test_elementwise_loop_misaligned_view_and_short_tensor():
+    n = 100_001
+    dev = torch.device("cuda", 0)
+    base = torch.arange(n + 3, dtype=torch.float32, device=dev)
+    out = torch.zeros(n + 3, dtype=torch.float32, device=dev)
+    # views starting at element 1 (not on a 16-byte boundary): lane path
+    tx = DeviceTensor(_Root(base, 0, 0, n + 3, _lib.PMX_F32), 1, (n,), "float")
+    ty = DeviceTensor(_Root(out, 1, 0, n + 3, _lib.PMX_F32), 1, (n,), "float")
+    P.eval_loop(n, P.lam("i", P.tensor_set(ty, ["i"], P.addf(P.tensor_get(tx, ["i"]), 0.5))))
+    default_ctx().check_errors()
+    o = out.cpu().numpy()
+    assert o[0] == 0 and np.array_equal(o[1:n + 1], np.arange(1, n + 1, dtype=np.float32) + 0.5)
+    # loop longer than the tensor: the first out-of-bounds iteration is reported
+    short = _tensor(torch.zeros(n - 10, dtype=torch.float32, device=dev), 2)
+    with pytest.raises(P.Diagnostics, match="out of bounds") as ei:
+        P.accelerate(lambda: P.eval_loop(n, P.lam("i", P.tensor_set(short, ["i"], 1.0))))
+    assert f"iteration {n - 10})" in str(ei.value)
+
+
+def test_elementwise_loop_error_index():
+    n = N
+    dev = torch.device("cuda", 0)
+    x = torch.ones(n, dtype=torch.int64, device=dev)
+    x[123_457] = 0
+    y = torch.zeros(n, dtype=torch.int64, device=dev)
+    tx = DeviceTensor(_Root(x, 0, 0, n, _lib.PMX_I64), 0, (n,), "int")
+    ty = DeviceTensor(_Root(y, 1, 0, n, _lib.PMX_I64), 0, (n,), "int")
+    with pytest.raises(P.Diagnostics, match="integer division by zero") as ei:
+        P.accelerate(lambda: P.eval_loop(n, P.lam("i", P.tensor_set(ty, ["i"], P.divi(5, P.tensor_get(tx, ["i"]))))))
+    assert "iteration 123457)" in str(ei.value)

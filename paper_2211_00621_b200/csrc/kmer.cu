@@ -14,6 +14,7 @@
 // reads it with L2-only loads (ld.global.cg), and normalises lazily: step t
 // multiplies by 1/c_{t-1} while computing a_t, and accumulates log c_t in
 // fp64.  Small S (alpha fits in shared memory) uses a shared-memory variant.
+#include <stdlib.h>
 #include "common.cuh"
 
 namespace pmx {
@@ -87,6 +88,94 @@ k_kmer_fwd(int kmer, float p_stay, float p_step, const float* __restrict__ E_lin
     }
 }
 
+// L2 policy: keep the alpha slices resident (evict_last); the emission table
+// is read once per step and may go first.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float4 ld_keep4(const float* a, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_keep(const float* a, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_keep4(float* a, float4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                 :: "l"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+
+// Global-alpha path, 4 states per thread: j = 4q .. 4q+3 share the step
+// predecessors (j >> 2 = q): alpha[q | b << (2k-2)], b = 0..3 — four scalar
+// loads, coalesced across the warp (consecutive q) and reused by the four
+// states; the stay terms, emissions and the new alpha are 16-byte vectors.
+// Same arithmetic per state as k_kmer_fwd (fmaf(p_stay, a_j, p_step *
+// ((a1 + a2) + (a3 + a4)))).
+__global__ void __launch_bounds__(1024)
+k_kmer_fwd_vec(int kmer, float p_stay, float p_step, const float* __restrict__ E_lin,
+               const int* __restrict__ obs, int64_t nsig, int T, double* __restrict__ out_ll,
+               float* __restrict__ ws) {
+    __shared__ float s_red[32];
+    __shared__ float s_c;
+    const int S = 1 << (2 * kmer);
+    const int Q = S >> 2;
+    const int hi = 2 * kmer - 2;
+    const uint64_t pol = l2_policy_evict_last();
+    float* bufA = ws + (int64_t)blockIdx.x * 2 * S;
+    float* bufB = bufA + S;
+    for (int64_t sig = blockIdx.x; sig < nsig; sig += gridDim.x) {
+        const int* o = obs + sig * (int64_t)T;
+        double ll = 0.0;
+        float inv = 1.0f / (float)S;
+        float* cur = bufA;
+        float* nxt = bufB;
+        for (int t = 0; t < T; ++t) {
+            const float* e = E_lin + (int64_t)o[t] * S;
+            float part = 0.f;
+            for (int q = threadIdx.x; q < Q; q += blockDim.x) {
+                const float4 ev = __ldg(reinterpret_cast<const float4*>(e) + q);
+                float4 v;
+                if (t == 0) {
+                    v = make_float4(inv * ev.x, inv * ev.y, inv * ev.z, inv * ev.w);
+                } else {
+                    const float4 a0 = ld_keep4(cur + 4 * q, pol);
+                    const float a1 = ld_keep(cur + q, pol);
+                    const float a2 = ld_keep(cur + (q | (1 << hi)), pol);
+                    const float a3 = ld_keep(cur + (q | (2 << hi)), pol);
+                    const float a4 = ld_keep(cur + (q | (3 << hi)), pol);
+                    const float st = p_step * ((a1 + a2) + (a3 + a4));
+                    v.x = inv * ev.x * fmaf(p_stay, a0.x, st);
+                    v.y = inv * ev.y * fmaf(p_stay, a0.y, st);
+                    v.z = inv * ev.z * fmaf(p_stay, a0.z, st);
+                    v.w = inv * ev.w * fmaf(p_stay, a0.w, st);
+                }
+                st_keep4(nxt + 4 * q, v, pol);
+                part += (v.x + v.y) + (v.z + v.w);
+            }
+            for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+            if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = part;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                float c = 0.f;
+                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) c += s_red[w];
+                s_c = c;
+                ll += log((double)c);
+            }
+            __syncthreads();
+            inv = 1.0f / s_c;
+            float* tmp = cur; cur = nxt; nxt = tmp;
+        }
+        if (threadIdx.x == 0) out_ll[sig] = ll;
+        __syncthreads();
+    }
+}
+
 }  // namespace pmx
 
 using namespace pmx;
@@ -123,7 +212,11 @@ int pmx_hmm_kmer_forward_f32(int32_t kmer, float p_stay, float p_step, const flo
     } else {
         // one CTA per SM keeps all alpha slices L2-resident (148 x 512 KiB)
         const unsigned grid = (unsigned)(nsig < sm_count() ? nsig : sm_count());
-        k_kmer_fwd<false><<<grid, threads, 0, st>>>(kmer, p_stay, p_step, E_lin, obs, nsig, T, out_ll, alpha);
+        static const bool old = getenv("PMX_KMER_SCALAR") && getenv("PMX_KMER_SCALAR")[0] == '1';
+        if (old || S < 4096)
+            k_kmer_fwd<false><<<grid, threads, 0, st>>>(kmer, p_stay, p_step, E_lin, obs, nsig, T, out_ll, alpha);
+        else
+            k_kmer_fwd_vec<<<grid, 1024, 0, st>>>(kmer, p_stay, p_step, E_lin, obs, nsig, T, out_ll, alpha);
     }
     PMX_CHECK_LAUNCH("kmer_fwd");
     return 0;

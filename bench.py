@@ -313,11 +313,23 @@ def bench_generic_skeletons(x, n, args, dist, peaks) -> dict:
              ("map2 (lam a b. a*b - a)", lambda: P.eval_map2(g, xs, ys), 12),
              ("reduce addf 0.0 (map (lam x. x*x))", lambda: P.eval_reduce(P.addf, 0.0, P.eval_map(sq, xs)), 4),
              ("loop n (lam i. tensorSet y [i] (2*(tensorGet x [i])+1))", lambda: P.eval_loop(n, body), 8)]
+    # seqLoop: 20 on-device steps of a 2-point stencil over 2^24 fp64 states
+    # (16 B per element-step: state read + write; the neighbour read hits cache)
+    ms_, steps_ = 1 << 24, 20
+    s_state = DeviceSeq(torch.arange(ms_, dtype=torch.float64, device=x.device) % 97, (ms_,), _lib.PMX_F64)
+    stencil = P.lam("x", "j", "t", P.mulf(0.5, P.addf("x", P.get(P.PREV, P.modi(P.addi("j", 1), ms_)))))
+    cases.append(("seq_loop 20 (lam x j t. 0.5*(x + get prev ((j+1) mod m))), m=2^24 fp64",
+                  lambda: P.seq_loop(steps_, stencil, s_state), None))
     out = {}
     c0, l0 = _lib.jit_stats()
     for name, fn, bpe in cases:
         ms, _ = device_time(fn, args.steps, 3, dist)
         ms /= args.steps
+        if bpe is None:      # seqLoop: 16 B per element-step over ms_ x steps_
+            gbs = 16.0 * ms_ * steps_ / (ms * 1e-3) / 1e9
+            out[name] = {"ms": round(ms, 4), "bytes_per_elem_step": 16, "GB/s": round(gbs, 1),
+                         "frac": round(gbs / peaks["hbm_gbs"], 3), "elem_steps_per_s": ms_ * steps_ / (ms * 1e-3)}
+            continue
         gbs = bpe * n / (ms * 1e-3) / 1e9
         out[name] = {"ms": round(ms, 4), "bytes_per_elem": bpe, "GB/s": round(gbs, 1),
                      "frac": round(gbs / peaks["hbm_gbs"], 3), "elem_per_s": n / (ms * 1e-3)}

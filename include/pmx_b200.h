@@ -192,7 +192,8 @@ PMX_API int pmx_fold(const pmx_program* op, const void* x, int32_t x_dtype, int6
 PMX_API int pmx_loop(const pmx_program* body, int64_t n, uint64_t* err, void* stream);
 
 /* seqLoop: persistent on-device iteration of a parallel step.
- * state has m elements (fp64); for t in [0,steps):
+ * state has m elements (fp64), scratch m + 8 (the tail holds the grid-barrier
+ * word of the specialised kernel); for t in [0,steps):
  *     state'[j] = f(state[j], j, t)   where f may GET from the previous state
  *                                     through arrays[0] (set by the library).
  * One launch, grid-wide barrier between steps.   (recursion used as a

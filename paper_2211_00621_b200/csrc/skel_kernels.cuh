@@ -420,6 +420,48 @@ k_loop_lanes(int64_t n, const B body, uint64_t* err) {
     }
 }
 
+// ---- seqLoop: persistent on-device iteration --------------------------------
+// state'[j] = f(state[j], j, t) for t in [0, steps), f reading the previous
+// state through arrays[0]; one resident wave of CTAs, a software grid barrier
+// (monotonic arrival counter, zeroed by the host) between steps.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+template <class F>
+__global__ void __launch_bounds__(256)
+k_seq_loop_jit(const F f, double* a, double* b, int64_t m, int64_t steps, unsigned* bar, uint64_t* err) {
+    F fl = f;
+    fl.T[0].offset = 0;
+    fl.T[0].shape[0] = m;
+    fl.T[0].rank = 1;
+    fl.T[0].dtype = PMX_F64;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = 0; t < steps; ++t) {
+        double* cur = (t & 1) ? b : a;
+        double* nxt = (t & 1) ? a : b;
+        fl.T[0].data = cur;
+        for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
+            const int64_t x[1] = {__double_as_longlong(__ldcg(cur + j))}, jj[1] = {j}, tt[1] = {t};
+            int64_t o[1];
+            int code[1] = {0};
+            fl.template run<1>(x, jj, tt, o, code);
+            if (code[0]) raise_err(err, j, code[0]);
+            nxt[j] = F::kOutFloat ? __longlong_as_double(o[0]) : (double)o[0];
+        }
+        grid_barrier(bar, (unsigned)(gridDim.x * (t + 1)));
+    }
+}
+
 // ---- elementwise parallel loop (tensor accesses at [i] only) ----------------
 // Packets of 4 consecutive iterations with vector loads/stores (B::vec), VP
 // packets per thread interleaved statement by statement; the < 4 tail

@@ -643,6 +643,20 @@ int pmx_seq_loop(const pmx_program* f, double* state, double* scratch, int64_t m
     PMX_REQUIRE(f->n_arrays >= 1, "pmx_seq_loop: program must reserve arrays[0] for the state");
     if (m <= 0 || steps <= 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
+    // run-time specialised persistent kernel (jit.cu); its grid-barrier word is
+    // the 8-byte slot after the m scratch values (scratch holds m + 8 doubles)
+    {
+        unsigned* bar = reinterpret_cast<unsigned*>(scratch + m);
+        int jr = jit_seq_loop(f, state, scratch, m, steps, bar, err, st);
+        if (jr < 0) return jr;
+        if (jr == 0) {
+            if (steps & 1) {
+                k_copy_f64<<<grid_for(m, 256, 4), 256, 0, st>>>(scratch, state, m);
+                PMX_CHECK_LAUNCH("seq_loop copy");
+            }
+            return 0;
+        }
+    }
     int dev = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_seq_loop, 256, 0);

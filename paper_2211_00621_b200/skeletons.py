@@ -506,7 +506,7 @@ def seq_loop(n: int, f, state, ctx: Optional[Ctx] = None, span: Span = NO_SPAN) 
     ctx = ctx or default_ctx()
     s = _materialize(_as_seq(state, "seqLoop", span))
     a = s.data.to(torch.float64).clone()
-    b = torch.empty_like(a)
+    b = torch.empty(a.numel() + 8, dtype=torch.float64, device=a.device)   # + grid-barrier word
     prog = _compile(f, ["float", "int", "int"], span, state_array=PREV)
     err = ctx.new_err(span)
     rc = _lib.load().pmx_seq_loop(C.byref(prog.program), a.data_ptr(), b.data_ptr(), a.numel(), int(n),

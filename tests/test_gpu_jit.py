@@ -201,3 +201,25 @@ def test_elementwise_loop_error_index():
     with pytest.raises(P.Diagnostics, match="integer division by zero") as ei:
         P.accelerate(lambda: P.eval_loop(n, P.lam("i", P.tensor_set(ty, ["i"], P.divi(5, P.tensor_get(tx, ["i"]))))))
     assert "iteration 123457)" in str(ei.value)
+
+
+def test_seq_loop_specialised_persistent_kernel():
+    # seqLoop above the threshold: run-time specialised persistent kernel with
+    # a software grid barrier per step; odd step count (result in scratch,
+    # copied back), neighbour reads through the previous state
+    m, steps = (1 << 16) + 5, 7
+    s0 = np.arange(m, dtype=np.float64) % 97
+    step = P.lam("x", "j", "t", P.mulf(0.5, P.addf("x", P.get(P.PREV, P.modi(P.addi("j", 1), m)))))
+    before = _launched()
+    got = np.asarray(P.accelerate(lambda s: P.seq_loop(steps, step, s), s0))
+    assert _launched() > before
+    want = s0.copy()
+    for _ in range(steps):
+        want = 0.5 * (want + np.roll(want, -1))
+    assert np.array_equal(got, want)
+    # an error in step 3 at element 4242 (division by zero) is reported
+    bad = P.lam("x", "j", "t", P.match(P.eqi("t", 3), True,
+                                       P.divf("x", P.int2float(P.subi("j", 4242))), "x"))
+    with pytest.raises(P.Diagnostics, match="float division by zero") as ei:
+        P.accelerate(lambda s: P.seq_loop(steps, bad, s), s0)
+    assert "element 4242)" in str(ei.value)

@@ -69,6 +69,13 @@ def main():
     ty = DeviceTensor(ry, 0, (n,), "float")
     body = P.lam("i", P.tensor_set(ty, ["i"], P.addf(P.mulf(2.0, P.tensor_get(tx, ["i"])), 1.0)))
     rep("loop y[i] = 2x[i]+1", timeit(lambda: P.eval_loop(n, body)), 8)
+    ms_, st_ = 1 << 24, 20
+    s_state = DeviceSeq(torch.arange(ms_, dtype=torch.float64, device=dev) % 97, (ms_,), _lib.PMX_F64)
+    stencil = P.lam("x", "j", "t", P.mulf(0.5, P.addf("x", P.get(P.PREV, P.modi(P.addi("j", 1), ms_)))))
+    t_ms = timeit(lambda: P.seq_loop(st_, stencil, s_state), reps=3, warm=1)
+    gbs = 16.0 * ms_ * st_ / (t_ms * 1e-3) / 1e9
+    print(json.dumps({"case": "seq_loop 20 steps m=2^24 f64", "ms": round(t_ms, 3), "GB/s": round(gbs, 1),
+                      "frac": round(gbs / peak, 3)}), flush=True)
     ctx.check_errors()
     torch.cuda.synchronize()
     ref = x.double() * 2 + 1

@@ -1,0 +1,312 @@
+// HMM forward on the tensor cores, CTA-pair variant: the two CTAs of a
+// cluster share 64 signals and split the OUTPUT STATES (CTA r owns states
+// [512 r, 512 r + 512)).  Same recursion, scaling and fp16 operands as
+// hmm_tc.cu (see there for the reference anchor and the precision argument).
+//
+// Why: the single-CTA kernel is bound by shared-memory bytes — every SM
+// streams the whole 2 MiB A^T through smem each step (TMA write + UMMA read)
+// for its 32 signals.  Here each SM streams only the A^T rows of its own 512
+// output states (1 MiB) for 64 signals, so A bytes per signal-step halve; the
+// u operand (64 signals x 1024 states, 128 KiB fp16) is held by both CTAs.
+//
+// Per step t (u_{t-1} complete in both CTAs' B buffers):
+//   MMA warp   : 4 M-blocks x 16 K-blocks of UMMA M=128 (states) N=64
+//                (signals) K=64, A^T tiles through a 3-stage TMA ring, two
+//                accumulator sets (even/odd K blocks), commit -> dfull.
+//   epilogue   : (8 warps: TMEM lane quadrant x signal half)
+//     a. wait dfull(t); arrive on the PEER's peer_done (my MMAs of t are done);
+//        wait my peer_done (the peer's MMAs of t are done: it no longer reads
+//        u_{t-1} in my region of its buffer, and my copy of u_{t-1} landed)
+//     b. u_t for my 512 states -> my region of my own B buffer (in place),
+//        per-signal partial sums of u_t
+//     c. partial sums -> the peer (st.async, completes tx on its psum barrier)
+//     d. bulk copy of my region (64 KiB) into the peer's B buffer (completes
+//        tx on the peer's uready); arrive.expect_tx on my uready for the
+//        peer's copy into mine
+//     e. wait psum: c_t = own + peer partials, 1/c_t, ll += log c_t
+//   MMA(t+1) waits my uready (my epilogue's arrival + the peer's copy).
+#include <cuda_fp16.h>
+#include <stdlib.h>
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace pmx {
+
+constexpr int HP_N = 64;             // signals per pair (UMMA N)
+constexpr int HP_M = 128;            // states per UMMA M block
+constexpr int HP_KB = 64;            // fp16 per 128-byte swizzle row
+constexpr int HP_S = 1024;
+constexpr int HP_HALF = HP_S / 2;    // output states per CTA
+constexpr int HP_MB = HP_HALF / HP_M;   // 4 M blocks per CTA
+constexpr int HP_NKB = HP_S / HP_KB;    // 16 K blocks
+constexpr int HP_ST = 3;             // TMA ring stages
+constexpr int HP_KMAX = 8;
+constexpr int HP_THREADS = 384;      // 4 control warps + 8 epilogue warps
+constexpr uint32_t HP_TILE = HP_M * 128;                 // 16 KiB A^T tile
+constexpr uint32_t HP_REGION = (HP_NKB / 2) * HP_N * 128;  // 64 KiB: one CTA's K blocks of u
+
+struct __align__(1024) HpSmem {
+    __half U[HP_NKB][HP_N * HP_KB];      // B operand: K-major SW128 [kblock][signal][64]
+    __half At[HP_ST][HP_M * HP_KB];      // A operand tiles
+    float E[HP_KMAX][HP_S];
+    float wsum[4][HP_N];
+    float psum_in[2][HP_N];              // the peer's partial sums (by step parity)
+    float inv_c[HP_N];
+    int sym[HP_N];
+    uint64_t full[HP_ST], empty[HP_ST];
+    uint64_t dfull, uready, peer_done, psum;
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t mapa_peer(uint32_t smem_addr, uint32_t peer) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(peer));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t remote_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}"
+        :: "r"(tc::smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+                 :: "r"(remote_addr), "r"(__float_as_uint(v)), "r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t remote_dst, const void* src, uint32_t bytes,
+                                                  uint32_t remote_bar) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(remote_dst), "r"(tc::smem_u32(src)), "r"(bytes), "r"(remote_bar) : "memory");
+}
+
+__device__ __forceinline__ uint32_t hp_u_offset(int s, int i) {
+    const int kb = i / HP_KB;
+    const uint32_t byte = (uint32_t)(i % HP_KB) * 2u;
+    const uint32_t chunk = (byte >> 4) ^ (uint32_t)(s & 7);
+    return (uint32_t)kb * (HP_N * 128) + (uint32_t)s * 128 + (chunk << 4) + (byte & 15);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HP_THREADS, 1)
+k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ E_lin,
+               const float* __restrict__ pi_lin, int K, const int* __restrict__ obs, int64_t nsig, int T,
+               double* __restrict__ out_ll) {
+    constexpr float kOut = 1.f / 1024.f, kSum = 1.f / 1024.f, kInit = 1048576.f;
+    extern __shared__ uint8_t smem_raw[];
+    HpSmem& Sm = *reinterpret_cast<HpSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_ctarank();
+    const uint32_t peer = rank ^ 1u;
+    const int64_t s0 = (int64_t)(blockIdx.x >> 1) * HP_N;
+    const int j0 = (int)rank * HP_HALF;              // first output state of this CTA
+
+    for (int v = threadIdx.x; v < K * HP_S; v += blockDim.x) (&Sm.E[0][0])[v] = E_lin[v];
+    if (threadIdx.x < HP_N) Sm.inv_c[threadIdx.x] = 1.f;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < HP_ST; ++s) { tc::mbar_init(&Sm.full[s], 1); tc::mbar_init(&Sm.empty[s], 1); }
+        tc::mbar_init(&Sm.dfull, 1);
+        // uready: two arrivals (armed with the peer copy's bytes; own u written) + the copy's tx
+        tc::mbar_init(&Sm.uready, 2);
+        tc::mbar_init(&Sm.peer_done, 1);
+        tc::mbar_init(&Sm.psum, 1);
+        tc::fence_mbar_init();
+        tc::tma_prefetch(&tmA);
+        // arm step 0 before any peer can deliver (the cluster barrier below orders it)
+        tc::mbar_arrive_expect_tx(&Sm.psum, HP_N * 4);
+        if (T > 1) tc::mbar_arrive_expect_tx(&Sm.uready, HP_REGION);
+    }
+    if (warp == 2) tc::tmem_alloc(&Sm.tmem_base, 512);
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    tc::tc_fence_after();
+    const uint32_t tmem = Sm.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {                                     // ---- TMA producer
+            int stage = 0; uint32_t phase = 0;
+            for (int t = 1; t < T; ++t)
+                for (int kb = 0; kb < HP_NKB; ++kb)
+                    for (int mb = 0; mb < HP_MB; ++mb) {
+                        tc::mbar_wait(&Sm.empty[stage], phase ^ 1);
+                        tc::mbar_arrive_expect_tx(&Sm.full[stage], HP_TILE);
+                        tc::tma_load_2d(Sm.At[stage], &tmA, &Sm.full[stage], kb * HP_KB, j0 + mb * HP_M);
+                        if (++stage == HP_ST) { stage = 0; phase ^= 1; }
+                    }
+        }
+    } else if (warp == 1) {                                  // ---- MMA issuer
+        constexpr uint32_t idesc = tc::instr_desc(HP_M, HP_N, 0);
+        int stage = 0; uint32_t phase = 0, upar = 0;
+        const uint64_t u_desc = tc::sw128_kmajor_desc(tc::smem_u32(&Sm.U[0][0]));
+        const uint64_t at_desc = tc::sw128_kmajor_desc(tc::smem_u32(Sm.At[0]));
+        for (int t = 1; t < T; ++t) {
+            tc::mbar_wait(&Sm.uready, upar); upar ^= 1;      // u_{t-1} complete (own half + peer's copy)
+            tc::tc_fence_after();
+            for (int kb = 0; kb < HP_NKB; ++kb)
+                for (int mb = 0; mb < HP_MB; ++mb) {
+                    tc::mbar_wait(&Sm.full[stage], phase);
+                    tc::tc_fence_after();
+                    if (tc::elect_one()) {
+                        const uint64_t ad = at_desc + (uint64_t)(stage * (HP_TILE >> 4));
+                        const uint64_t bd = u_desc + (uint64_t)(kb * ((HP_N * 128) >> 4));
+                        const uint32_t d = tmem + (uint32_t)((kb & 1) * (HP_MB * HP_N) + mb * HP_N);
+#pragma unroll
+                        for (int kk = 0; kk < HP_KB / 16; ++kk)
+                            tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb >= 2) || (kk != 0));
+                        tc::umma_commit(&Sm.empty[stage]);
+                    }
+                    __syncwarp();
+                    if (++stage == HP_ST) { stage = 0; phase ^= 1; }
+                }
+            if (tc::elect_one()) tc::umma_commit(&Sm.dfull);
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // ---- epilogue: warp w reads TMEM lane quadrant q = w % 4 (state
+        // j0 + mb*128 + 32q + lane), signals h*32 .. h*32+31 (h = (w-4)/4)
+        const int q = warp & 3;
+        const int ew = warp - 4;
+        const int h = ew >> 2;
+        const bool lead = threadIdx.x == 128;
+        double ll = 0.0;                                     // thread ew*32+lane < 64 owns signal
+        uint32_t dpar = 0, ppar = 0, spar = 0;
+        const float* Ef = &Sm.E[0][0];
+        const uint32_t peer_uready = mapa_peer(tc::smem_u32(&Sm.uready), peer);
+        const uint32_t peer_done_bar = mapa_peer(tc::smem_u32(&Sm.peer_done), peer);
+        const uint32_t peer_psum_bar = mapa_peer(tc::smem_u32(&Sm.psum), peer);
+        const uint32_t region_off = rank * HP_REGION;       // my K blocks of u
+        const uint32_t peer_region = mapa_peer(tc::smem_u32(&Sm.U[0][0]) + region_off, peer);
+        for (int t = 0; t < T; ++t) {
+            if (ew < 2) {
+                const int m = ew * 32 + lane;
+                const int64_t sg = s0 + m;
+                Sm.sym[m] = (sg < nsig) ? obs[sg * T + t] : 0;
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (t > 0) {
+                tc::mbar_wait(&Sm.dfull, dpar); dpar ^= 1;
+                tc::tc_fence_after();
+                if (lead) {
+                    // uready(t-1) completed before my MMAs of t ran: arm step t for the
+                    // peer's copy, then let the peer overwrite my region of its buffer
+                    if (t + 1 < T) tc::mbar_arrive_expect_tx(&Sm.uready, HP_REGION);
+                    mbar_arrive_remote(peer_done_bar);
+                }
+                mbar_wait_cluster(&Sm.peer_done, ppar); ppar ^= 1;
+            }
+            float ic[32], csum[32];
+            int eoff[32];
+#pragma unroll
+            for (int s = 0; s < 32; ++s) {
+                eoff[s] = Sm.sym[h * 32 + s] * HP_S;
+                ic[s] = Sm.inv_c[h * 32 + s] * kOut;
+                csum[s] = 0.f;
+            }
+#pragma unroll 1
+            for (int mb = 0; mb < HP_MB; ++mb) {
+                const int j = j0 + mb * HP_M + q * 32 + lane;
+                float d[32];
+                if (t > 0) {
+                    uint32_t r[32], r2[32];
+                    const uint32_t col = (uint32_t)(mb * HP_N + h * 32);
+                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + col, r);
+                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + HP_MB * HP_N + col, r2);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int s = 0; s < 32; ++s) d[s] = __uint_as_float(r[s]) + __uint_as_float(r2[s]);
+                } else {
+                    const float p = pi_lin[j] * kInit;
+#pragma unroll
+                    for (int s = 0; s < 32; ++s) d[s] = p;
+                }
+                const uint32_t byte = (uint32_t)(j % HP_KB) * 2u;
+                const uint32_t chunkj = byte >> 4;
+                uint8_t* rowp = reinterpret_cast<uint8_t*>(&Sm.U[0][0]) + (j / HP_KB) * (HP_N * 128) + (byte & 15);
+#pragma unroll
+                for (int s = 0; s < 32; ++s) {
+                    const int sg = h * 32 + s;
+                    const __half ur = __float2half_rn(d[s] * Ef[eoff[s] + j] * ic[s]);
+                    csum[s] += __half2float(ur);
+                    *reinterpret_cast<__half*>(rowp + sg * 128 + ((chunkj ^ (uint32_t)(sg & 7)) << 4)) = ur;
+                }
+            }
+            // per-signal sums over the warp's 32 states: transpose-reduce 32
+            // values over 32 lanes (lane l ends with signal h*32 + l)
+#pragma unroll
+            for (int w = 16; w > 0; w >>= 1) {
+                const bool upper = (lane & w) != 0;
+#pragma unroll
+                for (int s = 0; s < w; ++s) {
+                    const float send = upper ? csum[s] : csum[s + w];
+                    const float keep = upper ? csum[s + w] : csum[s];
+                    csum[s] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+                }
+            }
+            Sm.wsum[q][h * 32 + lane] = csum[0];
+            tc::fence_proxy_async();                 // u_t visible to the async proxy (UMMA, bulk copy)
+            tc::tc_fence_before();
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            float part = 0.f;
+            if (ew < 2) {                            // this CTA's partial of signal m
+                const int m = ew * 32 + lane;
+                part = (Sm.wsum[0][m] + Sm.wsum[1][m]) + (Sm.wsum[2][m] + Sm.wsum[3][m]);
+                st_async_f32(mapa_peer(tc::smem_u32(&Sm.psum_in[t & 1][m]), peer), part, peer_psum_bar);
+            }
+            if (lead && t + 1 < T) {
+                tc::mbar_arrive(&Sm.uready);                                // my own u_t is written
+                bulk_copy_to_peer(peer_region, reinterpret_cast<const uint8_t*>(&Sm.U[0][0]) + region_off,
+                                  HP_REGION, peer_uready);
+            }
+            if (ew < 2) {
+                mbar_wait_cluster(&Sm.psum, spar);
+                const int m = ew * 32 + lane;
+                // own + peer, added in rank order so both CTAs get the same c_t
+                const float c = (rank == 0 ? part + Sm.psum_in[t & 1][m] : Sm.psum_in[t & 1][m] + part) * kSum;
+                Sm.inv_c[m] = 1.f / c;
+                ll += log((double)c);
+            }
+            spar ^= 1;
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            // arm the next step's partial-sum exchange (the peer can only send it
+            // after my next peer_done arrival)
+            if (lead && t + 1 < T) tc::mbar_arrive_expect_tx(&Sm.psum, HP_N * 4);
+        }
+        if (rank == 0 && ew < 2 && s0 + ew * 32 + lane < nsig) out_ll[s0 + ew * 32 + lane] = ll;
+    }
+    tc::tc_fence_before();
+    tc::cluster_sync();                      // no CTA leaves while the peer may still write into it
+    if (warp == 2) tc::tmem_dealloc(tmem, 512);
+}
+
+bool make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t rows,
+                  uint64_t cols, uint32_t box_rows, uint32_t box_cols, CUtensorMapSwizzle swz);
+template <class ET>
+__global__ void k_hmm_tc_prep(const float* __restrict__ A, const float* __restrict__ log_E,
+                              const float* __restrict__ log_pi, int S, int K, ET* __restrict__ At,
+                              float* __restrict__ E_lin, float* __restrict__ pi_lin);
+
+int hmm_pair_launch(const float* log_pi, const float* A, const float* log_E, int S, int K, const int* obs,
+                    int64_t nsig, int T, double* out_ll, void* ws, cudaStream_t st) {
+    __half* At = (__half*)ws;
+    float* E_lin = (float*)((char*)ws + (size_t)S * S * 4);
+    float* pi_lin = E_lin + (size_t)HP_KMAX * S;
+    k_hmm_tc_prep<__half><<<dim3(S / 32, S / 32), dim3(32, 8), 0, st>>>(A, log_E, log_pi, S, K, At, E_lin, pi_lin);
+    PMX_CHECK_LAUNCH("hmm_pair_prep");
+    CUtensorMap tmA;
+    if (!make_tmap_2d(&tmA, At, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (uint64_t)S, (uint64_t)S, HP_M, HP_KB,
+                      CU_TENSOR_MAP_SWIZZLE_128B)) {
+        set_last_error("hmm_pair: cuTensorMapEncodeTiled failed");
+        return -2;
+    }
+    const unsigned grid = (unsigned)(2 * ((nsig + HP_N - 1) / HP_N));
+    const size_t smem = sizeof(HpSmem) + 1024;
+    cudaFuncSetAttribute(k_hmm_fwd_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_hmm_fwd_pair<<<grid, HP_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
+    PMX_CHECK_LAUNCH("hmm_fwd_pair");
+    return 0;
+}
+
+}  // namespace pmx

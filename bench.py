@@ -481,7 +481,9 @@ def bench_hmm(args, dist, peaks) -> dict:
     total, per = device_time(step, s, w, dist)
     ms = total / s
     flops = 2.0 * S * S * (T - 1) * nsig
-    smem_step = 2 * 2 * S * S + (S // 128) * S * 32 * 2      # A^T write + read (fp16) + B re-reads
+    # CTA-pair kernel: per SM per step, half of A^T written (TMA) + read (UMMA)
+    # in fp16, plus the 64-signal u tile re-read for each of its 4 M blocks
+    smem_step = 2 * 2 * (S // 2) * S + (S // 2 // 128) * S * 64 * 2
     return {"config": "4096 signals x 10^4 steps x 1024 states, K=8, fp16 operands / fp32 accumulate + fp64 log-scale",
             "element": "signal", "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms,
             "steps": s, "warmup": w,
@@ -493,10 +495,11 @@ def bench_hmm(args, dist, peaks) -> dict:
                          "smem_bytes_per_sm_per_step": smem_step,
                          "smem_B_per_clk_per_sm": smem_step * (T - 1) / (ms * 1e-3) / 1.965e9,
                          "smem_frac": smem_step * (T - 1) / (ms * 1e-3) / 1.965e9 / 128.0,
-                         "note": "tcgen05 kind::f16 (2^10-scaled fp16 operands, fp32 TMEM accumulation), 32 signals "
-                                 "per CTA, TMA multicast of A^T tiles across 4-CTA clusters, fp64 log-scale; per step "
-                                 "every SM writes (TMA) + reads (UMMA) the 2 MiB A^T and re-reads 512 KiB of u: "
-                                 "smem_frac is that traffic against 128 B/clk/SM"},
+                         "note": "tcgen05 kind::f16 (2^10-scaled fp16 operands, fp32 TMEM accumulation); CTA pairs "
+                                 "(cluster of 2) split the output states of 64 signals, exchanging u halves by "
+                                 "smem->peer bulk copy; UMMAs of step t+1 overlap the epilogue of step t (TMEM D "
+                                 "double-buffered); per step every SM writes + reads half of A^T (1 MiB each) and "
+                                 "re-reads 512 KiB of u: smem_frac is that traffic against 128 B/clk/SM"},
             "_ll": out.to("cpu").numpy()}
 
 

@@ -55,6 +55,7 @@ struct __align__(1024) HpSmem {
     int sym[HP_N];
     uint64_t full[HP_ST], empty[HP_ST];
     uint64_t dfull, uready, peer_done, psum;
+    uint64_t ublk[HP_MB];                // OVL: my u_t rows of M block mb written
     uint32_t tmem_base;
 };
 
@@ -91,6 +92,11 @@ __device__ __forceinline__ uint32_t hp_u_offset(int s, int i) {
     return (uint32_t)kb * (HP_N * 128) + (uint32_t)s * 128 + (chunk << 4) + (byte & 15);
 }
 
+// OVL: the UMMAs of step t+1 overlap the epilogue of step t.  D is double
+// buffered in TMEM by step parity (one accumulator set each), the K blocks of
+// a step run in the order my region (as my epilogue releases its M blocks,
+// barrier ublk[mb]) then the peer's region (after its bulk copy, uready).
+template <bool OVL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HP_THREADS, 1)
 k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ E_lin,
                const float* __restrict__ pi_lin, int K, const int* __restrict__ obs, int64_t nsig, int T,
@@ -110,7 +116,8 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         for (int s = 0; s < HP_ST; ++s) { tc::mbar_init(&Sm.full[s], 1); tc::mbar_init(&Sm.empty[s], 1); }
         tc::mbar_init(&Sm.dfull, 1);
         // uready: two arrivals (armed with the peer copy's bytes; own u written) + the copy's tx
-        tc::mbar_init(&Sm.uready, 2);
+        tc::mbar_init(&Sm.uready, OVL ? 1 : 2);
+        for (int b = 0; b < HP_MB; ++b) tc::mbar_init(&Sm.ublk[b], 1);
         tc::mbar_init(&Sm.peer_done, 1);
         tc::mbar_init(&Sm.psum, 1);
         tc::fence_mbar_init();
@@ -129,8 +136,10 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         if (lane == 0) {                                     // ---- TMA producer
             int stage = 0; uint32_t phase = 0;
             for (int t = 1; t < T; ++t)
-                for (int kb = 0; kb < HP_NKB; ++kb)
+                for (int ki = 0; ki < HP_NKB; ++ki)
                     for (int mb = 0; mb < HP_MB; ++mb) {
+                        // K block order: mine first (OVL), then the peer's
+                        const int kb = OVL ? (ki < HP_NKB / 2 ? (int)rank * 8 + ki : (int)peer * 8 + ki - 8) : ki;
                         tc::mbar_wait(&Sm.empty[stage], phase ^ 1);
                         tc::mbar_arrive_expect_tx(&Sm.full[stage], HP_TILE);
                         tc::tma_load_2d(Sm.At[stage], &tmA, &Sm.full[stage], kb * HP_KB, j0 + mb * HP_M);
@@ -143,24 +152,51 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         const uint64_t u_desc = tc::sw128_kmajor_desc(tc::smem_u32(&Sm.U[0][0]));
         const uint64_t at_desc = tc::sw128_kmajor_desc(tc::smem_u32(Sm.At[0]));
         for (int t = 1; t < T; ++t) {
-            tc::mbar_wait(&Sm.uready, upar); upar ^= 1;      // u_{t-1} complete (own half + peer's copy)
-            tc::tc_fence_after();
-            for (int kb = 0; kb < HP_NKB; ++kb)
+            if (!OVL) {
+                tc::mbar_wait(&Sm.uready, upar); upar ^= 1;  // u_{t-1} complete (own half + peer's copy)
+                tc::tc_fence_after();
+            }
+            const uint32_t dbase = OVL ? tmem + (uint32_t)((t & 1) * (HP_MB * HP_N)) : tmem;
+            for (int ki = 0; ki < HP_NKB; ++ki) {
+                int kb = ki;
+                if (OVL) {
+                    if (ki < HP_NKB / 2) {
+                        kb = (int)rank * 8 + ki;
+                        if ((ki & 1) == 0) {                      // my M block ki/2 of u_{t-1} written
+                            tc::mbar_wait(&Sm.ublk[ki >> 1], (uint32_t)((t - 1) & 1));
+                            tc::tc_fence_after();
+                        }
+                    } else {
+                        kb = (int)peer * 8 + ki - 8;
+                        if (ki == HP_NKB / 2) {                   // the peer's half of u_{t-1} landed
+                            tc::mbar_wait(&Sm.uready, upar); upar ^= 1;
+                            tc::tc_fence_after();
+                        }
+                    }
+                }
                 for (int mb = 0; mb < HP_MB; ++mb) {
                     tc::mbar_wait(&Sm.full[stage], phase);
                     tc::tc_fence_after();
                     if (tc::elect_one()) {
                         const uint64_t ad = at_desc + (uint64_t)(stage * (HP_TILE >> 4));
                         const uint64_t bd = u_desc + (uint64_t)(kb * ((HP_N * 128) >> 4));
-                        const uint32_t d = tmem + (uint32_t)((kb & 1) * (HP_MB * HP_N) + mb * HP_N);
+                        if (OVL) {
+                            const uint32_t d = dbase + (uint32_t)(mb * HP_N);
 #pragma unroll
-                        for (int kk = 0; kk < HP_KB / 16; ++kk)
-                            tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb >= 2) || (kk != 0));
+                            for (int kk = 0; kk < HP_KB / 16; ++kk)
+                                tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, (ki > 0) || (kk != 0));
+                        } else {
+                            const uint32_t d = tmem + (uint32_t)((kb & 1) * (HP_MB * HP_N) + mb * HP_N);
+#pragma unroll
+                            for (int kk = 0; kk < HP_KB / 16; ++kk)
+                                tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb >= 2) || (kk != 0));
+                        }
                         tc::umma_commit(&Sm.empty[stage]);
                     }
                     __syncwarp();
                     if (++stage == HP_ST) { stage = 0; phase ^= 1; }
                 }
+            }
             if (tc::elect_one()) tc::umma_commit(&Sm.dfull);
             __syncwarp();
         }
@@ -209,7 +245,14 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
             for (int mb = 0; mb < HP_MB; ++mb) {
                 const int j = j0 + mb * HP_M + q * 32 + lane;
                 float d[32];
-                if (t > 0) {
+                if (t > 0 && OVL) {
+                    uint32_t r[32];
+                    const uint32_t col = (uint32_t)((t & 1) * (HP_MB * HP_N) + mb * HP_N + h * 32);
+                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + col, r);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int s = 0; s < 32; ++s) d[s] = __uint_as_float(r[s]);
+                } else if (t > 0) {
                     uint32_t r[32], r2[32];
                     const uint32_t col = (uint32_t)(mb * HP_N + h * 32);
                     tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + col, r);
@@ -231,6 +274,12 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     const __half ur = __float2half_rn(d[s] * Ef[eoff[s] + j] * ic[s]);
                     csum[s] += __half2float(ur);
                     *reinterpret_cast<__half*>(rowp + sg * 128 + ((chunkj ^ (uint32_t)(sg & 7)) << 4)) = ur;
+                }
+                if (OVL && t + 1 < T) {                      // release M block mb of u_t to my MMA
+                    tc::fence_proxy_async();
+                    tc::tc_fence_before();
+                    asm volatile("bar.sync 1, 256;" ::: "memory");
+                    if (lead) tc::mbar_arrive(&Sm.ublk[mb]);
                 }
             }
             // per-signal sums over the warp's 32 states: transpose-reduce 32
@@ -256,7 +305,7 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 st_async_f32(mapa_peer(tc::smem_u32(&Sm.psum_in[t & 1][m]), peer), part, peer_psum_bar);
             }
             if (lead && t + 1 < T) {
-                tc::mbar_arrive(&Sm.uready);                                // my own u_t is written
+                if (!OVL) tc::mbar_arrive(&Sm.uready);                      // my own u_t is written
                 bulk_copy_to_peer(peer_region, reinterpret_cast<const uint8_t*>(&Sm.U[0][0]) + region_off,
                                   HP_REGION, peer_uready);
             }
@@ -303,8 +352,14 @@ int hmm_pair_launch(const float* log_pi, const float* A, const float* log_E, int
     }
     const unsigned grid = (unsigned)(2 * ((nsig + HP_N - 1) / HP_N));
     const size_t smem = sizeof(HpSmem) + 1024;
-    cudaFuncSetAttribute(k_hmm_fwd_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_hmm_fwd_pair<<<grid, HP_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
+    static const bool serial = getenv("PMX_HMM_PAIR_SERIAL") && getenv("PMX_HMM_PAIR_SERIAL")[0] == '1';
+    if (serial) {
+        cudaFuncSetAttribute(k_hmm_fwd_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_hmm_fwd_pair<false><<<grid, HP_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
+    } else {
+        cudaFuncSetAttribute(k_hmm_fwd_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_hmm_fwd_pair<true><<<grid, HP_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
+    }
     PMX_CHECK_LAUNCH("hmm_fwd_pair");
     return 0;
 }

@@ -51,9 +51,13 @@ def generic(reps=2):
     ty = DeviceTensor(_Root(yt, 1, 0, n, _lib.PMX_F32), 0, (n,), "float")
     f = P.lam("x", P.addf(P.mulf("x", "x"), 1.0))
     body = P.lam("i", P.tensor_set(ty, ["i"], P.addf(P.mulf(2.0, P.tensor_get(tx, ["i"])), 1.0)))
+    ms_ = 1 << 24
+    s_state = DeviceSeq(torch.arange(ms_, dtype=torch.float64, device="cuda") % 97, (ms_,), _lib.PMX_F64)
+    stencil = P.lam("x", "j", "t", P.mulf(0.5, P.addf("x", P.get(P.PREV, P.modi(P.addi("j", 1), ms_)))))
     for _ in range(reps):
         P.eval_map(f, xs).materialize()
         P.eval_loop(n, body)
+        P.seq_loop(20, stencil, s_state)
     torch.cuda.synchronize()
 
 

@@ -186,6 +186,18 @@ PMX_API int pmx_fold(const pmx_program* op, const void* x, int32_t x_dtype, int6
              void* workspace, size_t workspace_bytes,
              uint64_t* err, void* stream);
 
+/* Row functions: out[r] = fold over row r of x (rows delimited by int64
+ * offsets[nrows+1]) — `map (lam row. reduce op acc (map g row)) rows`,
+ * `foldl op acc row` and `reduce op acc row` (g == NULL).  Inside a map body
+ * the reference runs these sequentially (interp.py:82-84): a left fold from
+ * init in element order.  g: r0 = x, r1 = index in the row; op: r0 = acc,
+ * r1 = value.  out has out_dtype; errors report the row index.
+ *                                     replaces eval_map over [[a]] with a row
+ *                                     function, interp.py:294-304 + 322-343 */
+PMX_API int pmx_map_rows_fold(const pmx_program* g, const pmx_program* op, const void* x, int32_t x_dtype,
+                      const int64_t* offsets, int64_t nrows, const void* init_host, void* out,
+                      int32_t out_dtype, uint64_t* err, void* stream);
+
 /* Parallel loop: body(i) for i in [0,n), effects through TSET on the tensor
  * views in body->arrays (already rebased into their device roots by the
  * host's marshal_in, Alg. 2).           replaces eval_loop interp.py:346-358 */

@@ -27,7 +27,7 @@ from .runtime import (
 )
 from .skeletons import (
     PREV, Ctx, LazyMap, accelerate, device_call, eval_loop, eval_map, eval_map2, eval_reduce, flatten,
-    fold, seq_loop,
+    fold, map_rows_fold, seq_loop,
 )
 from .casestudies import hmm_forward, hmm_kmer_forward, knn_classify, nn_gradients, rk4_sweep, rk4_trace, viterbi
 

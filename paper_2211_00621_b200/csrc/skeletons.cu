@@ -292,6 +292,40 @@ __global__ void k_fold_seq(const __grid_constant__ pmx_program OP, const void* x
     *out = acc;
 }
 
+// map (lam row. reduce op acc (map g row)) rows — and foldl op acc row, reduce
+// op acc row: one thread per row, the inner fold sequential in element order
+// (inside a map body the reference's skeletons run sequentially,
+// interp.py:82-84, so the fold is a left fold from acc).  g sees (x, index in
+// the row), op sees (acc, x).  Errors report the row (the map's element).
+__global__ void k_rows_fold_vm(const __grid_constant__ pmx_program G, int has_g,
+                               const __grid_constant__ pmx_program OP, const void* x, int xt,
+                               const int64_t* __restrict__ offs, int64_t nrows, int64_t init,
+                               void* out, int ot, uint64_t* err) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += stride) {
+        int64_t acc = init;
+        int code = 0;
+        const int64_t lo = offs[r], hi = offs[r + 1];
+        for (int64_t e = lo; e < hi && !code; ++e) {
+            int64_t R[PMX_MAX_REGS];
+            int64_t v = load_elem(x, xt, e);
+            if (has_g) {
+                R[0] = v;
+                R[1] = e - lo;
+                code = vm_run(G, R);
+                if (code) break;
+                v = vm_opnd(G, R, G.out);
+            }
+            R[0] = acc;
+            R[1] = v;
+            code = vm_run(OP, R);
+            if (!code) acc = vm_opnd(OP, R, OP.out);
+        }
+        if (!code && !store_elem(out, ot, r, acc)) code = PMX_E_F32_RANGE;
+        if (code) raise_err(err, r, code);
+    }
+}
+
 __global__ void k_loop_vm(const __grid_constant__ pmx_program P, int64_t n, uint64_t* err) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -623,6 +657,22 @@ int pmx_fold(const pmx_program* op, const void* x, int32_t xt, int64_t n,
     memcpy(&init, init_host, 8);
     k_fold_seq<<<1, 32, 0, (cudaStream_t)stream>>>(*op, x, xt, n, init, (int64_t*)out, err);
     PMX_CHECK_LAUNCH("fold");
+    return 0;
+}
+
+int pmx_map_rows_fold(const pmx_program* g, const pmx_program* op, const void* x, int32_t xt,
+                      const int64_t* offsets, int64_t nrows, const void* init_host, void* out, int32_t out_dtype,
+                      uint64_t* err, void* stream) {
+    PMX_REQUIRE(op && init_host && offsets && out, "pmx_map_rows_fold: null argument");
+    PMX_REQUIRE(nrows >= 0, "pmx_map_rows_fold: negative row count");
+    if (nrows == 0) return 0;
+    int64_t init;
+    memcpy(&init, init_host, 8);
+    pmx_program none;
+    memset(&none, 0, sizeof(none));
+    k_rows_fold_vm<<<grid_for(nrows, 128, 8), 128, 0, (cudaStream_t)stream>>>(
+        g ? *g : none, g ? 1 : 0, *op, x, xt, offsets, nrows, init, out, out_dtype, err);
+    PMX_CHECK_LAUNCH("rows_fold");
     return 0;
 }
 

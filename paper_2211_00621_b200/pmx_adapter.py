@@ -48,6 +48,54 @@ def to_lam(f, n_params: int, syn, rt, host_array: Callable) -> L.Lam:
     return L.Lam(params, body)
 
 
+def to_row_fold(f, syn, rt, host_array: Callable):
+    """A row function of `map` over a sequence of sequences:
+        lam row. foldl op acc row  |  lam row. reduce op acc row
+      | lam row. reduce op acc (map g row)
+    -> (g Lam or None, op Lam, acc).  Anything else is Unsupported."""
+    S = syn
+    if not isinstance(f, rt.Closure):
+        raise Unsupported("row function")
+    tr = _Translator(syn, rt, host_array)
+    scope = {"__env__": f.env}
+    row = f.param
+
+    def is_row(x):
+        return isinstance(x, S.Var) and x.name == row
+
+    e = f.body
+    g_e = None
+    if isinstance(e, S.ReduceE):
+        op_e, acc_e = e.fn, e.acc
+        if isinstance(e.seq, S.MapE) and is_row(e.seq.seq):
+            g_e = e.seq.fn
+        elif not is_row(e.seq):
+            raise Unsupported("row function: reduce over something other than the row")
+    else:
+        head, args = e, []
+        while isinstance(head, S.App):
+            args.append(head.arg)
+            head = head.fn
+        args.reverse()
+        if not (isinstance(head, S.ConstE) and isinstance(head.const, S.CBuiltin) and head.const.name == "foldl"
+                and len(args) == 3 and is_row(args[2])):
+            raise Unsupported("row function (expected foldl / reduce over the row)")
+        op_e, acc_e = args[0], args[1]
+
+    def fn_lam(fe, n):
+        params = [f"_r{i}" for i in range(n)]
+        body = tr.apply_value(tr.expr(fe, scope, 0), [L.Var(p) for p in params], depth=1)
+        return L.Lam(params, tr.as_expr(body))
+
+    op_lam = fn_lam(op_e, 2)
+    g_lam = fn_lam(g_e, 1) if g_e is not None else None
+    acc = tr.expr(acc_e, scope, 0)
+    if not isinstance(acc, L.Const):
+        raise Unsupported("row function: accumulator must be a constant or captured scalar")
+    v = acc.value
+    return g_lam, op_lam, (bool(v) if acc.ty == "bool" else v)
+
+
 class _Fn:
     """A function value during translation: Closure, builtin partial, or a
     lambda bound in the body being translated."""
@@ -338,9 +386,36 @@ def install(interp):
             t.copy_back()
         return out
 
+    def run_rows(f, s, ctx, span):
+        written: list = []
+
+        def host_array(v):
+            if isinstance(v, rt.TensorView):
+                t = HeapTensor(v, ctx.heap.buffers[v.buffer])
+                written.append(t)
+                return t
+            return seq_to_device(v)
+        try:
+            g, op, acc = to_row_fold(f, syn, rt, host_array)
+        except (Unsupported, CompileError) as exc:
+            raise rt.runtime_error(f"not supported on the B200 device: {exc}", span) from None
+        dctx = K.Ctx()
+        dctx.device = True
+        K._ctx_stack.append(dctx)
+        try:
+            out = to_ref(K.map_rows_fold(g, op, acc, seq_to_device(s)))
+            dctx.check_errors()
+        except B200Diagnostics as d:
+            raise rt.runtime_error(d.items[0].message, span) from None
+        finally:
+            K._ctx_stack.pop()
+        return out
+
     def eval_map(f, s, ctx, span):
         if not ctx.run_parallel or not s:
             return orig["eval_map"](f, s, ctx, span)
+        if isinstance(s[0], list):                  # row function over [[a]]
+            return run_rows(f, s, ctx, span)
         _elem_type(s)
         return run(f, 1, ctx, span, lambda lam: to_ref(K._materialize(K.eval_map(lam, seq_to_device(s)))))
 

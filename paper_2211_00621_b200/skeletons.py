@@ -477,6 +477,45 @@ def fold(f, acc, s, ctx: Optional[Ctx] = None, span: Span = NO_SPAN):
     return DeviceScalar(out, acc_t == "float", err, span)
 
 
+# ------------------------------------------------------------ row folds
+
+def map_rows_fold(g, op, acc, s, ctx: Optional[Ctx] = None, span: Span = NO_SPAN) -> DeviceSeq:
+    """map (lam row. reduce op acc (map g row)) s over a sequence of sequences
+    (g=None: `foldl op acc row` / `reduce op acc row`).  Inside a map body the
+    reference runs the inner skeletons sequentially (pmx/interp.py:82-84), so
+    each row is a left fold from `acc` in element order (interp.py:322-325)."""
+    ctx = ctx or default_ctx()
+    s = _materialize(_as_seq(s, "map", span))
+    if isinstance(s, DeviceRecordSeq):
+        raise runtime_error("map over records supports field projections (lam p. p.l)", span)
+    if s.offsets is not None:
+        nrows, offs = len(s), s.offsets
+    elif s.rank == 2:
+        nrows, m = s.shape
+        offs = torch.arange(nrows + 1, dtype=torch.int64, device=_device()) * m
+    else:
+        raise runtime_error("a row function needs a sequence of sequences", span)
+    if isinstance(acc, DeviceScalar):
+        acc = acc.get()
+    acc_t = "float" if isinstance(acc, float) else ("bool" if isinstance(acc, bool) else "int")
+    et = _elem_type(s)
+    gc = _compile(g, [et, "int"], span) if g is not None else None
+    vt = gc.out_type if gc is not None else et
+    opc = _compile(op, [acc_t, "int" if vt == "char" else vt], span)
+    if opc.out_type not in (acc_t, "never"):
+        raise runtime_error(f"fold: operator returns {opc.out_type}, accumulator is {acc_t}", span)
+    code = _lib.PMX_F64 if acc_t == "float" else (_lib.PMX_BOOL if acc_t == "bool" else _lib.PMX_I64)
+    out = torch.empty(nrows, dtype=_torch_dtype(code), device=_device())
+    init = _scalar_bits(acc, acc_t)
+    err = ctx.new_err(span)
+    rc = _lib.load().pmx_map_rows_fold(C.byref(gc.program) if gc is not None else None, C.byref(opc.program),
+                                       s.ptr(), s.dtype_code, offs.data_ptr(), nrows, C.byref(init),
+                                       out.data_ptr(), code, err.data_ptr(), ctx.stream_ptr())
+    _lib.check(rc, "map_rows_fold")
+    ctx.launches += 1
+    return DeviceSeq(out, (nrows,), code, elem_tag=acc_t)
+
+
 # ------------------------------------------------------------------ loop
 
 def eval_loop(n: int, f, ctx: Optional[Ctx] = None, span: Span = NO_SPAN) -> dict:

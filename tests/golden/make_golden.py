@@ -328,6 +328,18 @@ def record_adapter_constructs(corpus) -> dict:
         return out
 
     def eval_map(f, s, ctx, span):
+        if s and isinstance(s[0], list):              # row function over [[a]]
+            out = orig["eval_map"](f, s, ctx, span)
+            if ctx.run_parallel:
+                tensors: list = []
+                try:
+                    g, op, acc = pmx_adapter.to_row_fold(f, syn, rt, lambda v: ir_json.HostArray(conv(v), elem(v)))
+                    records.append(dict(kind="map_rows", g=ir_json.dump(g) if g is not None else None,
+                                        op=ir_json.dump(op), acc=acc, rows=[conv(r) for r in s],
+                                        x_elem=elem(s[0]), expected=out))
+                except pmx_adapter.Unsupported:
+                    pass
+            return out
         return rec("map", ctx, f, 1, lambda: orig["eval_map"](f, s, ctx, span), xs=conv(s), x_elem=elem(s)) \
             if s else orig["eval_map"](f, s, ctx, span)
 

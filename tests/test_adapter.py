@@ -14,7 +14,7 @@ REF = pathlib.Path("/root/reference/pkg")
 pytestmark = pytest.mark.skipif(not REF.exists(), reason="reference interpreter not available")
 
 # constructs the device cannot run: nested sequences as elements, recursion
-UNSUPPORTED = {"recursion_pow", "foldl_in_accel", "nested_map"}
+UNSUPPORTED = {"recursion_pow"}      # a recursive closure as the map function
 
 
 def _pmx():
@@ -64,6 +64,18 @@ def install_checker(interp):
     def eval_map(f, s, ctx, span):
         if not ctx.run_parallel or not s:
             return orig["eval_map"](f, s, ctx, span)
+        if isinstance(s[0], list):                   # row function: left fold per row
+            try:
+                g, op, acc = pmx_adapter.to_row_fold(f, syn, rt, lambda v: HostArray(conv(v), "int"))
+            except pmx_adapter.Unsupported as exc:
+                raise rt.runtime_error(f"not supported on the B200 device: {exc}", span) from None
+            out = []
+            for row in s:
+                a = acc
+                for x in conv(row):
+                    a = O.ir_apply(op, a, O.ir_apply(g, x) if g is not None else x)
+                out.append(a)
+            return out
         return O.ir_map(tr(f, 1, ctx, span), conv(s))
 
     @wrap

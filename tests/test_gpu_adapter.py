@@ -13,7 +13,7 @@ from conftest import GOLDEN
 from paper_2211_00621_b200 import _lib, ir_json
 from paper_2211_00621_b200.runtime import DeviceSeq, DeviceTensor, _Root, seq_to_device, seq_to_host, to_device
 from paper_2211_00621_b200.skeletons import (
-    Ctx, _ctx_stack, _materialize, eval_loop, eval_map, eval_map2, eval_reduce,
+    Ctx, _ctx_stack, _materialize, eval_loop, eval_map, eval_map2, eval_reduce, map_rows_fold,
 )
 
 pytestmark = pytest.mark.gpu
@@ -48,7 +48,7 @@ def _close(a, b, rel):
 def test_adapter_construct_on_device(rec):
     name, _, c, rel = rec
     rel = rel or 1e-12
-    lam, arrays = ir_json.load(c["lam"], _make_array)
+    lam, arrays = ir_json.load(c["lam"], _make_array) if "lam" in c else (None, [])
     ctx = Ctx()
     ctx.device = True
     _ctx_stack.append(ctx)
@@ -64,6 +64,11 @@ def test_adapter_construct_on_device(rec):
         elif kind == "reduce":
             got = eval_reduce(lam, c["acc"], _seq(c["xs"], c["x_elem"])).get()
             assert _close(got, c["expected"], rel), (got, c["expected"])
+        elif kind == "map_rows":          # row function over [[a]] (nested_map, foldl_in_accel)
+            g = ir_json.load(c["g"], _make_array)[0] if c["g"] is not None else None
+            op = ir_json.load(c["op"], _make_array)[0]
+            out = seq_to_host(map_rows_fold(g, op, c["acc"], seq_to_device(c["rows"]))).tolist()
+            assert all(_close(a, b, rel) for a, b in zip(out, c["expected"])), (out, c["expected"])
         elif kind == "loop":
             eval_loop(c["n"], lam)
             tensors = [a for a in arrays if isinstance(a, DeviceTensor)]
@@ -76,4 +81,5 @@ def test_adapter_construct_on_device(rec):
 
 
 def test_adapter_records_present():
-    assert len(RECORDS) >= 30
+    assert len(RECORDS) >= 35
+    assert {c["kind"] for _, _, c, _ in RECORDS} >= {"map", "map2", "reduce", "loop", "map_rows"}

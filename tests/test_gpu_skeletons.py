@@ -277,3 +277,25 @@ def test_seq_loop_persistent_iteration():
     for _ in range(50):
         ref = 0.5 * (ref + np.roll(ref, -1))
     assert np.allclose(got, ref, rtol=1e-14)
+
+
+def test_map_rows_fold_irregular_and_regular(jit_mode):
+    # map (lam row. reduce addi 0 (map (lam x. muli x x) row)) over irregular rows,
+    # foldl with a non-commutative operator (left fold order), float rows
+    from paper_2211_00621_b200 import map_rows_fold, subf
+    rows = [[1, 2, 3], [], [4], [5, 6, 7, 8]]
+    got = accelerate(lambda s: map_rows_fold(lam("x", muli("x", "x")), addi, 0, s), rows)
+    assert [int(v) for v in got] == [14, 0, 16, 174]
+    got = accelerate(lambda s: map_rows_fold(None, subi, 100, s), rows)
+    assert [int(v) for v in got] == [94, 100, 96, 74]
+    frows = [[0.5, 0.25, 0.125], [1.5, -2.0, 3.25]]
+    got = accelerate(lambda s: map_rows_fold(None, subf, 1.0, s), frows)
+    assert list(got) == [((1.0 - 0.5) - 0.25) - 0.125, ((1.0 - 1.5) + 2.0) - 3.25]
+
+
+def test_map_rows_fold_error_reports_row(jit_mode):
+    from paper_2211_00621_b200 import map_rows_fold
+    rows = [[1, 2], [3, 0], [0]]
+    with pytest.raises(Diagnostics, match="integer division by zero") as ei:
+        accelerate(lambda s: map_rows_fold(lam("x", divi(12, "x")), addi, 0, s), rows)
+    assert "element 1)" in str(ei.value)

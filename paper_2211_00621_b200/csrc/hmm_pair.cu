@@ -39,7 +39,8 @@ constexpr int HP_S = 1024;
 constexpr int HP_HALF = HP_S / 2;    // output states per CTA
 constexpr int HP_MB = HP_HALF / HP_M;   // 4 M blocks per CTA
 constexpr int HP_NKB = HP_S / HP_KB;    // 16 K blocks
-constexpr int HP_ST = 3;             // TMA ring stages
+constexpr int HP_ST = 5;             // TMA ring stages (the emission table is read through L1,
+                                     // leaving shared memory to the ring: 80 KiB of A^T in flight)
 constexpr int HP_KMAX = 8;
 constexpr int HP_THREADS = 384;      // 4 control warps + 8 epilogue warps
 constexpr uint32_t HP_TILE = HP_M * 128;                 // 16 KiB A^T tile
@@ -48,7 +49,6 @@ constexpr uint32_t HP_REGION = (HP_NKB / 2) * HP_N * 128;  // 64 KiB: one CTA's 
 struct __align__(1024) HpSmem {
     __half U[HP_NKB][HP_N * HP_KB];      // B operand: K-major SW128 [kblock][signal][64]
     __half At[HP_ST][HP_M * HP_KB];      // A operand tiles
-    float E[HP_KMAX][HP_S];
     float wsum[4][HP_N];
     float psum_in[2][HP_N];              // the peer's partial sums (by step parity)
     float inv_c[HP_N];
@@ -110,7 +110,6 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
     const int64_t s0 = (int64_t)(blockIdx.x >> 1) * HP_N;
     const int j0 = (int)rank * HP_HALF;              // first output state of this CTA
 
-    for (int v = threadIdx.x; v < K * HP_S; v += blockDim.x) (&Sm.E[0][0])[v] = E_lin[v];
     if (threadIdx.x < HP_N) Sm.inv_c[threadIdx.x] = 1.f;
     if (threadIdx.x == 0) {
         for (int s = 0; s < HP_ST; ++s) { tc::mbar_init(&Sm.full[s], 1); tc::mbar_init(&Sm.empty[s], 1); }
@@ -209,7 +208,7 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         const bool lead = threadIdx.x == 128;
         double ll = 0.0;                                     // thread ew*32+lane < 64 owns signal
         uint32_t dpar = 0, ppar = 0, spar = 0;
-        const float* Ef = &Sm.E[0][0];
+        const float* __restrict__ Ef = E_lin;
         const uint32_t peer_uready = mapa_peer(tc::smem_u32(&Sm.uready), peer);
         const uint32_t peer_done_bar = mapa_peer(tc::smem_u32(&Sm.peer_done), peer);
         const uint32_t peer_psum_bar = mapa_peer(tc::smem_u32(&Sm.psum), peer);
@@ -271,7 +270,7 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
 #pragma unroll
                 for (int s = 0; s < 32; ++s) {
                     const int sg = h * 32 + s;
-                    const __half ur = __float2half_rn(d[s] * Ef[eoff[s] + j] * ic[s]);
+                    const __half ur = __float2half_rn(d[s] * __ldg(Ef + eoff[s] + j) * ic[s]);
                     csum[s] += __half2float(ur);
                     *reinterpret_cast<__half*>(rowp + sg * 128 + ((chunkj ^ (uint32_t)(sg & 7)) << 4)) = ur;
                 }

@@ -45,6 +45,7 @@ constexpr int HP_KMAX = 8;
 constexpr int HP_THREADS = 384;      // 4 control warps + 8 epilogue warps
 constexpr uint32_t HP_TILE = HP_M * 128;                 // 16 KiB A^T tile
 constexpr uint32_t HP_REGION = (HP_NKB / 2) * HP_N * 128;  // 64 KiB: one CTA's K blocks of u
+constexpr uint32_t HP_CHUNK = 2 * HP_N * 128;              // 16 KiB: the two K blocks of one M block
 
 struct __align__(1024) HpSmem {
     __half U[HP_NKB][HP_N * HP_KB];      // B operand: K-major SW128 [kblock][signal][64]
@@ -56,6 +57,7 @@ struct __align__(1024) HpSmem {
     uint64_t full[HP_ST], empty[HP_ST];
     uint64_t dfull, uready, peer_done, psum;
     uint64_t ublk[HP_MB];                // OVL: my u_t rows of M block mb written
+    uint64_t upeer[HP_MB];               // OVL: the peer's M block mb of u_t landed (bulk copy tx)
     uint32_t tmem_base;
 };
 
@@ -93,9 +95,10 @@ __device__ __forceinline__ uint32_t hp_u_offset(int s, int i) {
 }
 
 // OVL: the UMMAs of step t+1 overlap the epilogue of step t.  D is double
-// buffered in TMEM by step parity (one accumulator set each), the K blocks of
-// a step run in the order my region (as my epilogue releases its M blocks,
-// barrier ublk[mb]) then the peer's region (after its bulk copy, uready).
+// buffered in TMEM by step parity (one accumulator set each).  As the
+// epilogue finishes M block mb it releases those rows of u_t to its own UMMAs
+// (ublk[mb]) and bulk-copies them (16 KiB) to the peer (upeer[mb] there); the
+// K blocks of a step run per M block: mine, then the peer's.
 template <bool OVL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HP_THREADS, 1)
 k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ E_lin,
@@ -116,14 +119,16 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         tc::mbar_init(&Sm.dfull, 1);
         // uready: two arrivals (armed with the peer copy's bytes; own u written) + the copy's tx
         tc::mbar_init(&Sm.uready, OVL ? 1 : 2);
-        for (int b = 0; b < HP_MB; ++b) tc::mbar_init(&Sm.ublk[b], 1);
+        for (int b = 0; b < HP_MB; ++b) { tc::mbar_init(&Sm.ublk[b], 1); tc::mbar_init(&Sm.upeer[b], 1); }
         tc::mbar_init(&Sm.peer_done, 1);
         tc::mbar_init(&Sm.psum, 1);
         tc::fence_mbar_init();
         tc::tma_prefetch(&tmA);
         // arm step 0 before any peer can deliver (the cluster barrier below orders it)
         tc::mbar_arrive_expect_tx(&Sm.psum, HP_N * 4);
-        if (T > 1) tc::mbar_arrive_expect_tx(&Sm.uready, HP_REGION);
+        if (T > 1 && !OVL) tc::mbar_arrive_expect_tx(&Sm.uready, HP_REGION);
+        if (T > 1 && OVL)
+            for (int b = 0; b < HP_MB; ++b) tc::mbar_arrive_expect_tx(&Sm.upeer[b], HP_CHUNK);
     }
     if (warp == 2) tc::tmem_alloc(&Sm.tmem_base, 512);
     tc::tc_fence_before();
@@ -138,7 +143,9 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 for (int ki = 0; ki < HP_NKB; ++ki)
                     for (int mb = 0; mb < HP_MB; ++mb) {
                         // K block order: mine first (OVL), then the peer's
-                        const int kb = OVL ? (ki < HP_NKB / 2 ? (int)rank * 8 + ki : (int)peer * 8 + ki - 8) : ki;
+                        // OVL K block order: per M block g of the producing epilogue, my
+                        // two K blocks then the peer's two
+                        const int kb = OVL ? (int)((ki & 3) < 2 ? rank : peer) * 8 + 2 * (ki >> 2) + (ki & 1) : ki;
                         tc::mbar_wait(&Sm.empty[stage], phase ^ 1);
                         tc::mbar_arrive_expect_tx(&Sm.full[stage], HP_TILE);
                         tc::tma_load_2d(Sm.At[stage], &tmA, &Sm.full[stage], kb * HP_KB, j0 + mb * HP_M);
@@ -159,18 +166,14 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
             for (int ki = 0; ki < HP_NKB; ++ki) {
                 int kb = ki;
                 if (OVL) {
-                    if (ki < HP_NKB / 2) {
-                        kb = (int)rank * 8 + ki;
-                        if ((ki & 1) == 0) {                      // my M block ki/2 of u_{t-1} written
-                            tc::mbar_wait(&Sm.ublk[ki >> 1], (uint32_t)((t - 1) & 1));
-                            tc::tc_fence_after();
-                        }
-                    } else {
-                        kb = (int)peer * 8 + ki - 8;
-                        if (ki == HP_NKB / 2) {                   // the peer's half of u_{t-1} landed
-                            tc::mbar_wait(&Sm.uready, upar); upar ^= 1;
-                            tc::tc_fence_after();
-                        }
+                    const int g = ki >> 2, w = ki & 3;
+                    kb = (int)(w < 2 ? rank : peer) * 8 + 2 * g + (w & 1);
+                    if (w == 0) {                                 // my M block g of u_{t-1} written
+                        tc::mbar_wait(&Sm.ublk[g], (uint32_t)((t - 1) & 1));
+                        tc::tc_fence_after();
+                    } else if (w == 2) {                          // the peer's M block g landed
+                        tc::mbar_wait(&Sm.upeer[g], (uint32_t)((t - 1) & 1));
+                        tc::tc_fence_after();
                     }
                 }
                 for (int mb = 0; mb < HP_MB; ++mb) {
@@ -225,9 +228,15 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 tc::mbar_wait(&Sm.dfull, dpar); dpar ^= 1;
                 tc::tc_fence_after();
                 if (lead) {
-                    // uready(t-1) completed before my MMAs of t ran: arm step t for the
-                    // peer's copy, then let the peer overwrite my region of its buffer
-                    if (t + 1 < T) tc::mbar_arrive_expect_tx(&Sm.uready, HP_REGION);
+                    // uready / upeer of step t-1 completed before my MMAs of t ran: arm
+                    // step t for the peer's copies, then let the peer overwrite my
+                    // region of its buffer
+                    if (t + 1 < T) {
+                        if (OVL)
+                            for (int b = 0; b < HP_MB; ++b) tc::mbar_arrive_expect_tx(&Sm.upeer[b], HP_CHUNK);
+                        else
+                            tc::mbar_arrive_expect_tx(&Sm.uready, HP_REGION);
+                    }
                     mbar_arrive_remote(peer_done_bar);
                 }
                 mbar_wait_cluster(&Sm.peer_done, ppar); ppar ^= 1;
@@ -278,7 +287,14 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     tc::fence_proxy_async();
                     tc::tc_fence_before();
                     asm volatile("bar.sync 1, 256;" ::: "memory");
-                    if (lead) tc::mbar_arrive(&Sm.ublk[mb]);
+                    if (lead) {
+                        tc::mbar_arrive(&Sm.ublk[mb]);
+                        // this M block's two K blocks of u_t -> the peer (16 KiB)
+                        const uint32_t off = (uint32_t)(rank * 8 + 2 * mb) * (HP_N * 128);
+                        bulk_copy_to_peer(mapa_peer(tc::smem_u32(&Sm.U[0][0]) + off, peer),
+                                          reinterpret_cast<const uint8_t*>(&Sm.U[0][0]) + off, HP_CHUNK,
+                                          mapa_peer(tc::smem_u32(&Sm.upeer[mb]), peer));
+                    }
                 }
             }
             // per-signal sums over the warp's 32 states: transpose-reduce 32
@@ -303,8 +319,8 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 part = (Sm.wsum[0][m] + Sm.wsum[1][m]) + (Sm.wsum[2][m] + Sm.wsum[3][m]);
                 st_async_f32(mapa_peer(tc::smem_u32(&Sm.psum_in[t & 1][m]), peer), part, peer_psum_bar);
             }
-            if (lead && t + 1 < T) {
-                if (!OVL) tc::mbar_arrive(&Sm.uready);                      // my own u_t is written
+            if (!OVL && lead && t + 1 < T) {
+                tc::mbar_arrive(&Sm.uready);                                // my own u_t is written
                 bulk_copy_to_peer(peer_region, reinterpret_cast<const uint8_t*>(&Sm.U[0][0]) + region_off,
                                   HP_REGION, peer_uready);
             }

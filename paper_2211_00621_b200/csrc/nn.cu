@@ -67,19 +67,33 @@ k_nn_grad(const double* __restrict__ x, const int* __restrict__ y, const double*
         __syncthreads();                                   // previous tile's xs / dzs reads done
         const double* xt = x + p0 * nin;
         for (int v = tid; v < npt * nin; v += NN_THREADS) xs[v] = __ldcs(xt + v);   // coalesced stream
+        if (npt < TILE)                                    // tail tile: zero the unused rows
+            for (int v = npt * nin + tid; v < TILE * nin; v += NN_THREADS) xs[v] = 0.0;
         __syncthreads();
         // ---- per point: z (reference foldl order), softmax, loss, dz
         double z[PT];
 #pragma unroll
         for (int k = 0; k < PT; ++k) z[k] = bj;
-        for (int i = 0; i < nin; ++i) {
-            const double wij = act ? ws[i * nout + j] : 0.0;
+        // rows past the tile end hold zeros and are never used
+        const double* xr = xs + row * nin;
+        const double* wc = ws + (act ? j : 0);             // w[i][j]: lanes j contiguous
+        int i = 0;
+        if ((nin & 1) == 0) {                               // x as 16-byte pairs over i
+#pragma unroll 4
+            for (; i < nin; i += 2) {
+                const double w0 = wc[i * nout], w1 = wc[(i + 1) * nout];
 #pragma unroll
-            for (int k = 0; k < PT; ++k) {
-                const int pl = row + k * NP;
-                const double xv = pl < npt ? xs[pl * nin + i] : 0.0;
-                z[k] = __dadd_rn(z[k], __dmul_rn(xv, wij));
+                for (int k = 0; k < PT; ++k) {
+                    const double2 x2 = *reinterpret_cast<const double2*>(xr + k * NP * nin + i);
+                    z[k] = __dadd_rn(z[k], __dmul_rn(x2.x, w0));
+                    z[k] = __dadd_rn(z[k], __dmul_rn(x2.y, w1));
+                }
             }
+        }
+        for (; i < nin; ++i) {
+            const double wij = wc[i * nout];
+#pragma unroll
+            for (int k = 0; k < PT; ++k) z[k] = __dadd_rn(z[k], __dmul_rn(xr[k * NP * nin + i], wij));
         }
 #pragma unroll
         for (int k = 0; k < PT; ++k) {
@@ -110,9 +124,19 @@ k_nn_grad(const double* __restrict__ x, const int* __restrict__ y, const double*
             const int pr = tid + q * NN_THREADS;
             if (pr < npairs) {
                 const int ii = pr / nout, jj = pr % nout;
-                double a = dwacc[q];
-                for (int pl = 0; pl < npt; ++pl) a = __dadd_rn(a, __dmul_rn(xs[pl * nin + ii], dzs[pl * NN_MAXOUT + jj]));
-                dwacc[q] = a;
+                // two partial chains (even / odd points) halve the dependent-add
+                // depth; folded in order at the end of the tile
+                double a0 = 0.0, a1 = 0.0;
+                const double* xc = xs + ii;
+                const double* dc = dzs + jj;
+                int pl = 0;
+#pragma unroll 4
+                for (; pl + 1 < npt; pl += 2) {
+                    a0 = __dadd_rn(a0, __dmul_rn(xc[pl * nin], dc[pl * NN_MAXOUT]));
+                    a1 = __dadd_rn(a1, __dmul_rn(xc[(pl + 1) * nin], dc[(pl + 1) * NN_MAXOUT]));
+                }
+                if (pl < npt) a0 = __dadd_rn(a0, __dmul_rn(xc[pl * nin], dc[pl * NN_MAXOUT]));
+                dwacc[q] = __dadd_rn(dwacc[q], __dadd_rn(a0, a1));
             }
         }
     }

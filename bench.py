@@ -449,6 +449,7 @@ def bench_knn(args, dist, peaks) -> dict:
     flops = 2.0 * d * ntr * nq
     return {"config": "2^20 train x 2^16 queries, d=64, k=8, 10 classes, fp32", "element": "query",
             "value": nq * dist.world / (ms * 1e-3), "ms_per_step": ms, "steps": s, "warmup": w,
+            "pair_dims_per_s": float(ntr) * nq * d * dist.world / (ms * 1e-3),
             "roofline": {"bound": "TMEM read (one fp32 distance per candidate leaves TMEM)",
                          "achieved_tflops": flops / (ms * 1e-3) / 1e12,
                          "peak_tflops": peaks["bf16_tflops"],
@@ -504,6 +505,7 @@ def bench_hmm(args, dist, peaks) -> dict:
     return {"config": "4096 signals x 10^4 steps x 1024 states, K=8, fp16 operands / fp32 accumulate + fp64 log-scale",
             "element": "signal", "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms,
             "steps": s, "warmup": w,
+            "trellis_cells_per_s": float(S) * S * (T - 1) * nsig * dist.world / (ms * 1e-3),
             "roofline": {"bound": "shared memory (A^T streamed through smem every step)",
                          "achieved_tflops": flops / (ms * 1e-3) / 1e12,
                          "peak_tflops": peaks["bf16_tflops"],
@@ -687,6 +689,7 @@ def bench_kmer(args, dist, peaks) -> dict:
     return {"config": "S=65536 (k=8) de Bruijn, 1024 signals per GPU (8192 over 8), T=6000, fp32",
             "element": "signal", "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms,
             "steps": s, "warmup": w,
+            "trellis_cells_per_s": 5.0 * S * (T - 1) * nsig * dist.world / (ms * 1e-3),
             "roofline": {"bound": "L2 (alpha slices L2-resident, streamed every step)",
                          "achieved_l2_GBps": bytes_ / (ms * 1e-3) / 1e9,
                          "vs_hbm_peak": bytes_ / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],

@@ -326,10 +326,13 @@ def bench_generic_skeletons(x, n, args, dist, peaks) -> dict:
     g = P.lam("a", "b", P.subf(P.mulf("a", "b"), "a"))
     sq = P.lam("x", P.mulf("x", "x"))
     body = P.lam("i", P.tensor_set(ty, ["i"], P.addf(P.mulf(2.0, P.tensor_get(tx, ["i"])), 1.0)))
+    gop = P.lam("a", "b", P.addf("a", P.mulf("b", 1.0)))
     cases = [("map (lam x. x*x + 1)", lambda: P.eval_map(f, xs).materialize(), 8),
              ("map2 (lam a b. a*b - a)", lambda: P.eval_map2(g, xs, ys), 12),
              ("reduce addf 0.0 (map (lam x. x*x))", lambda: P.eval_reduce(P.addf, 0.0, P.eval_map(sq, xs)), 4),
-             ("loop n (lam i. tensorSet y [i] (2*(tensorGet x [i])+1))", lambda: P.eval_loop(n, body), 8)]
+             ("loop n (lam i. tensorSet y [i] (2*(tensorGet x [i])+1))", lambda: P.eval_loop(n, body), 8),
+             ("reduce (lam a b. addf a (mulf b 1.0)) 0.0 s  [operator not recognised: ordered tree]",
+              lambda: P.eval_reduce(gop, 0.0, xs), 4)]
     # seqLoop: 20 on-device steps of a 2-point stencil over 2^24 fp64 states
     # (16 B per element-step: state read + write; the neighbour read hits cache)
     ms_, steps_ = 1 << 24, 20

@@ -420,6 +420,126 @@ k_loop_lanes(int64_t n, const B body, uint64_t* err) {
     }
 }
 
+// ---- reduce with an arbitrary associative operator ---------------------------
+// fold op init (map f x) for an operator the library does not recognise: the
+// result must equal the sequential left fold for any associative op, so every
+// combine keeps the left operand earlier in the sequence.  A CTA owns a
+// contiguous range; per round each warp folds a contiguous 1024-element block
+// (each lane folds its 32 contiguous elements, read as 16-byte loads through
+// L1; an ordered shuffle tree — lower lane on the left — folds the lanes), the
+// 8 warp values fold in warp order into the CTA's running value; the last CTA
+// folds the CTA values in CTA order after `init`.
+struct OPart { int64_t v; int has; };
+
+template <class G>
+__device__ __forceinline__ OPart op_combine(const G& g, OPart a, OPart b, uint64_t* err, int64_t idx) {
+    if (!a.has) return b;
+    if (!b.has) return a;
+    const int64_t i0[1] = {a.v}, i1[1] = {b.v};
+    int64_t o[1];
+    int code[1] = {0};
+    g.template run<1>(i0, i1, o, code);
+    if (code[0]) raise_err(err, idx, code[0]);
+    OPart r;
+    r.v = o[0];
+    r.has = 1;
+    return r;
+}
+
+template <class TX, class F, class G>
+__global__ void __launch_bounds__(256, 4)
+k_reduce_ordered(const TX* __restrict__ x, int64_t n, const F f, const G g, int64_t init, int64_t* out,
+                 OPart* partials, unsigned* ticket, uint64_t* err) {
+    constexpr int UP = 8;                         // 16-byte packets per lane per round
+    constexpr int RW = 32 * 4 * UP;               // elements per warp per round
+    const int nw = blockDim.x >> 5;
+    const int64_t RB = (int64_t)nw * RW;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int64_t per = ((n + gridDim.x - 1) / gridDim.x + RB - 1) / RB * RB;
+    const int64_t lo = min(n, (int64_t)blockIdx.x * per), hi = min(n, lo + per);
+    __shared__ OPart s_w[32];
+    OPart acc;
+    acc.v = 0;
+    acc.has = 0;
+    for (int64_t r0 = lo; r0 < hi; r0 += RB) {
+        const int64_t wb = r0 + (int64_t)w * RW;
+        const int64_t p0 = wb + (int64_t)l * (4 * UP);
+        TX xe[UP][4];
+        const bool full = p0 + 4 * UP <= hi && ((uintptr_t)(x + p0) % (4 * sizeof(TX)) == 0);
+        if (full) {
+#pragma unroll
+            for (int u = 0; u < UP; ++u) {
+                Pack4<TX> v;
+#pragma unroll
+                for (int k = 0; k < (int)(sizeof(TX) >= 4 ? sizeof(TX) / 4 : 1); ++k)
+                    v.q[k] = __ldg(reinterpret_cast<const uint4*>(x + p0 + 4 * u) + k);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) xe[u][e] = v.e[e];
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < UP; ++u)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int64_t q = p0 + 4 * u + e;
+                    xe[u][e] = q < hi ? x[q] : x[lo];
+                }
+        }
+        OPart lp;
+        lp.v = 0;
+        lp.has = 0;
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+            typename F::Res r[4];
+            int code[4] = {0, 0, 0, 0};
+            f(xe[u], p0 + 4 * u, r, code);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int64_t q = p0 + 4 * u + e;
+                if (q >= hi) break;
+                if (code[e]) { raise_err(err, q, code[e]); continue; }
+                OPart v;
+                v.v = to_reg(r[e]);
+                v.has = 1;
+                lp = op_combine(g, lp, v, err, q);
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            OPart rr;
+            rr.v = __shfl_down_sync(0xffffffffu, lp.v, o);
+            rr.has = __shfl_down_sync(0xffffffffu, lp.has, o);
+            if ((l & (2 * o - 1)) == 0 && l + o < 32) lp = op_combine(g, lp, rr, err, p0);
+        }
+        if (l == 0) s_w[w] = lp;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int q = 0; q < nw; ++q) acc = op_combine(g, acc, s_w[q], err, r0);
+        __syncthreads();
+    }
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = acc;
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        OPart a;
+        a.v = init;
+        a.has = 1;                                   // init applied once, on the left
+        for (int b = 0; b < (int)gridDim.x; ++b) {
+            OPart q;
+            q.v = __ldcg(&partials[b].v);
+            q.has = __ldcg(&partials[b].has);
+            a = op_combine(g, a, q, err, n > 0 ? n - 1 : 0);
+        }
+        *out = a.v;
+        *ticket = 0u;
+    }
+}
+
 // ---- seqLoop: persistent on-device iteration --------------------------------
 // state'[j] = f(state[j], j, t) for t in [0, steps), f reading the previous
 // state through arrays[0]; one resident wave of CTAs, a software grid barrier

@@ -146,9 +146,12 @@ static int recognise_reduce(const pmx_program* op) {
         if (!((lo == 0 && hi == 1) || (lo == 1 && hi == 0))) return K_VM;
         bool picks_lhs = (S.b == lo && S.c == hi);   // cmp ? lo : hi
         if (!picks_lhs) return K_VM;
+        // Float forms must be exactly OMinF/OMaxF(acc, x) = acc CMP x ? acc : x
+        // (lo = acc): the mirrored form returns the other operand on ties, which
+        // differs for signed zeros and NaN. Int forms are equal either way.
         switch (C.op) {   // (lo < hi ? lo : hi) = min ; (lo > hi ? lo : hi) = max
-            case PMX_OP_LTF: return K_MIN_F;
-            case PMX_OP_GTF: return K_MAX_F;
+            case PMX_OP_LTF: return lo == 0 ? K_MIN_F : K_VM;
+            case PMX_OP_GTF: return lo == 0 ? K_MAX_F : K_VM;
             case PMX_OP_LTI: return K_MIN_I;
             case PMX_OP_GTI: return K_MAX_I;
         }
@@ -603,6 +606,10 @@ int pmx_map_reduce(const pmx_program* f, const pmx_program* op, const void* x, i
     const int okind = recognise_reduce(op);
     if (okind != K_VM && ((okind < K_ADD_I) == (acc_dtype == PMX_F64))) {
         r = jit_map_reduce(f, okind, x, xt, n, init_host, out, y, yt, ws, st, nullptr, err);
+        if (r <= 0) return r;
+    }
+    if (okind == K_VM && y == nullptr) {     // unrecognised operator: ordered specialised kernel
+        r = jit_reduce_generic(f, op, x, xt, n, init_host, acc_dtype, out, ws, st, err);
         if (r <= 0) return r;
     }
     // interpreter path

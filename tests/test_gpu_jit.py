@@ -223,3 +223,30 @@ def test_seq_loop_specialised_persistent_kernel():
     with pytest.raises(P.Diagnostics, match="float division by zero") as ei:
         P.accelerate(lambda s: P.seq_loop(steps, bad, s), s0)
     assert "element 4242)" in str(ei.value)
+
+
+def test_reduce_unrecognised_operator_is_an_ordered_fold():
+    # leftmost non-zero: associative, not commutative -> only an order-keeping
+    # tree gives the sequential answer
+    n = (1 << 20) + 13
+    x = np.zeros(n, dtype=np.int64)
+    x[777_777] = 5
+    x[900_001] = 9
+    x[3] = 0
+    first_nz = P.lam("a", "b", P.if_(P.eqi("a", 0), "b", "a"))
+    before = _launched()
+    got = P.accelerate(lambda s: P.eval_reduce(first_nz, 0, s), x)
+    assert _launched() > before
+    assert got == 5
+    x[123] = -4
+    assert P.accelerate(lambda s: P.eval_reduce(first_nz, 0, s), x) == -4
+    # generic map feeding a generic (sum written as two instructions) operator
+    xi = (np.arange(n, dtype=np.int64) % 1000) - 500
+    add2 = P.lam("a", "b", P.addi("a", P.muli("b", 1)))
+    sq = P.lam("v", P.muli("v", "v"))
+    got = P.accelerate(lambda s: P.eval_reduce(add2, 7, P.eval_map(sq, s)), xi)
+    assert got == 7 + int(np.sum(xi * xi))
+    # mirrored float max (not the recognised form): exact fold semantics
+    xf = np.random.default_rng(1).standard_normal(n)
+    mx = P.lam("a", "b", P.if_(P.gtf("b", "a"), "b", "a"))
+    assert P.accelerate(lambda s: P.eval_reduce(mx, -1e300, s), xf) == float(np.max(xf))

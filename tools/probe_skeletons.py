@@ -69,6 +69,8 @@ def main():
     ty = DeviceTensor(ry, 0, (n,), "float")
     body = P.lam("i", P.tensor_set(ty, ["i"], P.addf(P.mulf(2.0, P.tensor_get(tx, ["i"])), 1.0)))
     rep("loop y[i] = 2x[i]+1", timeit(lambda: P.eval_loop(n, body)), 8)
+    gop = P.lam("a", "b", P.addf("a", P.mulf("b", 1.0)))
+    rep("reduce generic op (ordered tree)", timeit(lambda: P.eval_reduce(gop, 0.0, xs)), 4)
     ms_, st_ = 1 << 24, 20
     s_state = DeviceSeq(torch.arange(ms_, dtype=torch.float64, device=dev) % 97, (ms_,), _lib.PMX_F64)
     stencil = P.lam("x", "j", "t", P.mulf(0.5, P.addf("x", P.get(P.PREV, P.modi(P.addi("j", 1), ms_)))))

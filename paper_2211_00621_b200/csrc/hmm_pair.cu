@@ -42,7 +42,9 @@ constexpr int HP_NKB = HP_S / HP_KB;    // 16 K blocks
 constexpr int HP_ST = 5;             // TMA ring stages (the emission table is read through L1,
                                      // leaving shared memory to the ring: 80 KiB of A^T in flight)
 constexpr int HP_KMAX = 8;
-constexpr int HP_THREADS = 384;      // 4 control warps + 8 epilogue warps
+constexpr int HP_EW = 8;             // epilogue warps (16 measured: 13.8 vs 13.4 us/step) (4 TMEM lane quadrants x HP_EW/4 signal groups)
+constexpr int HP_SPW = HP_N / (HP_EW / 4);   // signals per epilogue warp
+constexpr int HP_THREADS = 128 + 32 * HP_EW; // 4 control warps + the epilogue warps
 constexpr uint32_t HP_TILE = HP_M * 128;                 // 16 KiB A^T tile
 constexpr uint32_t HP_REGION = (HP_NKB / 2) * HP_N * 128;  // 64 KiB: one CTA's K blocks of u
 constexpr uint32_t HP_CHUNK = 2 * HP_N * 128;              // 16 KiB: the two K blocks of one M block
@@ -86,6 +88,9 @@ __device__ __forceinline__ void bulk_copy_to_peer(uint32_t remote_dst, const voi
     asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(remote_dst), "r"(tc::smem_u32(src)), "r"(bytes), "r"(remote_bar) : "memory");
 }
+
+__device__ __forceinline__ void tmem_ld_spw(uint32_t taddr, uint32_t (&r)[32]) { tc::tmem_ld_32x32b_x32(taddr, r); }
+__device__ __forceinline__ void tmem_ld_spw(uint32_t taddr, uint32_t (&r)[16]) { tc::tmem_ld_32x32b_x16(taddr, r); }
 
 __device__ __forceinline__ uint32_t hp_u_offset(int s, int i) {
     const int kb = i / HP_KB;
@@ -223,7 +228,7 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 const int64_t sg = s0 + m;
                 Sm.sym[m] = (sg < nsig) ? obs[sg * T + t] : 0;
             }
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" :: "n"(32 * HP_EW) : "memory");
             if (t > 0) {
                 tc::mbar_wait(&Sm.dfull, dpar); dpar ^= 1;
                 tc::tc_fence_after();
@@ -241,44 +246,44 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 }
                 mbar_wait_cluster(&Sm.peer_done, ppar); ppar ^= 1;
             }
-            float ic[32], csum[32];
-            int eoff[32];
+            float ic[HP_SPW], csum[HP_SPW];
+            int eoff[HP_SPW];
 #pragma unroll
-            for (int s = 0; s < 32; ++s) {
-                eoff[s] = Sm.sym[h * 32 + s] * HP_S;
-                ic[s] = Sm.inv_c[h * 32 + s] * kOut;
+            for (int s = 0; s < HP_SPW; ++s) {
+                eoff[s] = Sm.sym[h * HP_SPW + s] * HP_S;
+                ic[s] = Sm.inv_c[h * HP_SPW + s] * kOut;
                 csum[s] = 0.f;
             }
 #pragma unroll 1
             for (int mb = 0; mb < HP_MB; ++mb) {
                 const int j = j0 + mb * HP_M + q * 32 + lane;
-                float d[32];
+                float d[HP_SPW];
                 if (t > 0 && OVL) {
-                    uint32_t r[32];
-                    const uint32_t col = (uint32_t)((t & 1) * (HP_MB * HP_N) + mb * HP_N + h * 32);
-                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + col, r);
+                    uint32_t r[HP_SPW];
+                    const uint32_t col = (uint32_t)((t & 1) * (HP_MB * HP_N) + mb * HP_N + h * HP_SPW);
+                    tmem_ld_spw(tmem + ((uint32_t)(q * 32) << 16) + col, r);
                     tc::tmem_ld_wait();
 #pragma unroll
-                    for (int s = 0; s < 32; ++s) d[s] = __uint_as_float(r[s]);
+                    for (int s = 0; s < HP_SPW; ++s) d[s] = __uint_as_float(r[s]);
                 } else if (t > 0) {
-                    uint32_t r[32], r2[32];
-                    const uint32_t col = (uint32_t)(mb * HP_N + h * 32);
-                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + col, r);
-                    tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + HP_MB * HP_N + col, r2);
+                    uint32_t r[HP_SPW], r2[HP_SPW];
+                    const uint32_t col = (uint32_t)(mb * HP_N + h * HP_SPW);
+                    tmem_ld_spw(tmem + ((uint32_t)(q * 32) << 16) + col, r);
+                    tmem_ld_spw(tmem + ((uint32_t)(q * 32) << 16) + HP_MB * HP_N + col, r2);
                     tc::tmem_ld_wait();
 #pragma unroll
-                    for (int s = 0; s < 32; ++s) d[s] = __uint_as_float(r[s]) + __uint_as_float(r2[s]);
+                    for (int s = 0; s < HP_SPW; ++s) d[s] = __uint_as_float(r[s]) + __uint_as_float(r2[s]);
                 } else {
                     const float p = pi_lin[j] * kInit;
 #pragma unroll
-                    for (int s = 0; s < 32; ++s) d[s] = p;
+                    for (int s = 0; s < HP_SPW; ++s) d[s] = p;
                 }
                 const uint32_t byte = (uint32_t)(j % HP_KB) * 2u;
                 const uint32_t chunkj = byte >> 4;
                 uint8_t* rowp = reinterpret_cast<uint8_t*>(&Sm.U[0][0]) + (j / HP_KB) * (HP_N * 128) + (byte & 15);
 #pragma unroll
-                for (int s = 0; s < 32; ++s) {
-                    const int sg = h * 32 + s;
+                for (int s = 0; s < HP_SPW; ++s) {
+                    const int sg = h * HP_SPW + s;
                     const __half ur = __float2half_rn(d[s] * __ldg(Ef + eoff[s] + j) * ic[s]);
                     csum[s] += __half2float(ur);
                     *reinterpret_cast<__half*>(rowp + sg * 128 + ((chunkj ^ (uint32_t)(sg & 7)) << 4)) = ur;
@@ -286,7 +291,7 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 if (OVL && t + 1 < T) {                      // release M block mb of u_t to my MMA
                     tc::fence_proxy_async();
                     tc::tc_fence_before();
-                    asm volatile("bar.sync 1, 256;" ::: "memory");
+                    asm volatile("bar.sync 1, %0;" :: "n"(32 * HP_EW) : "memory");
                     if (lead) {
                         tc::mbar_arrive(&Sm.ublk[mb]);
                         // this M block's two K blocks of u_t -> the peer (16 KiB)
@@ -297,10 +302,15 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     }
                 }
             }
-            // per-signal sums over the warp's 32 states: transpose-reduce 32
-            // values over 32 lanes (lane l ends with signal h*32 + l)
+            // per-signal sums over the warp's 32 states: fold the lane halves while
+            // there are fewer signals than lanes, then transpose-reduce HP_SPW
+            // values over HP_SPW lanes (lane l < HP_SPW ends with signal h*HP_SPW + l)
 #pragma unroll
-            for (int w = 16; w > 0; w >>= 1) {
+            for (int w = 16; w >= HP_SPW; w >>= 1)
+#pragma unroll
+                for (int s = 0; s < HP_SPW; ++s) csum[s] += __shfl_xor_sync(0xffffffffu, csum[s], w);
+#pragma unroll
+            for (int w = HP_SPW / 2; w > 0; w >>= 1) {
                 const bool upper = (lane & w) != 0;
 #pragma unroll
                 for (int s = 0; s < w; ++s) {
@@ -309,10 +319,10 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     csum[s] = keep + __shfl_xor_sync(0xffffffffu, send, w);
                 }
             }
-            Sm.wsum[q][h * 32 + lane] = csum[0];
+            if (lane < HP_SPW) Sm.wsum[q][h * HP_SPW + lane] = csum[0];
             tc::fence_proxy_async();                 // u_t visible to the async proxy (UMMA, bulk copy)
             tc::tc_fence_before();
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" :: "n"(32 * HP_EW) : "memory");
             float part = 0.f;
             if (ew < 2) {                            // this CTA's partial of signal m
                 const int m = ew * 32 + lane;
@@ -333,7 +343,7 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 ll += log((double)c);
             }
             spar ^= 1;
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" :: "n"(32 * HP_EW) : "memory");
             // arm the next step's partial-sum exchange (the peer can only send it
             // after my next peer_done arrival)
             if (lead && t + 1 < T) tc::mbar_arrive_expect_tx(&Sm.psum, HP_N * 4);

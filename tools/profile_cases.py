@@ -54,10 +54,12 @@ def generic(reps=2):
     ms_ = 1 << 24
     s_state = DeviceSeq(torch.arange(ms_, dtype=torch.float64, device="cuda") % 97, (ms_,), _lib.PMX_F64)
     stencil = P.lam("x", "j", "t", P.mulf(0.5, P.addf("x", P.get(P.PREV, P.modi(P.addi("j", 1), ms_)))))
+    gop = P.lam("a", "b", P.addf("a", P.mulf("b", 1.0)))
     for _ in range(reps):
         P.eval_map(f, xs).materialize()
         P.eval_loop(n, body)
         P.seq_loop(20, stencil, s_state)
+        P.eval_reduce(gop, 0.0, xs)
     torch.cuda.synchronize()
 
 

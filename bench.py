@@ -450,8 +450,16 @@ def bench_knn(args, dist, peaks) -> dict:
     total, per = device_time(step, s, w, dist)
     ms = total / s
     flops = 2.0 * d * ntr * nq
+    # end to end through the public entry with host arrays (H2D of train,
+    # labels, queries + kernels + D2H of the labels)
+    import paper_2211_00621_b200 as P
+    hX, hQ, hL = X.cpu().pin_memory(), Q.cpu().pin_memory(), L.cpu().pin_memory()
+    e2e_ms, _ = host_time(lambda: P.accelerate(lambda a, b, q: P.knn_classify(a, b, q, k, c), hX, hL, hQ),
+                          2, 1, dist)
+    e2e = {"value": nq * dist.world / (e2e_ms / 2 * 1e-3), "unit": "queries/s",
+           "h2d_bytes_per_step": hX.numel() * 4 + hQ.numel() * 4 + hL.numel() * 4, "d2h_bytes_per_step": nq * 4}
     return {"config": "2^20 train x 2^16 queries, d=64, k=8, 10 classes, fp32", "element": "query",
-            "value": nq * dist.world / (ms * 1e-3), "ms_per_step": ms, "steps": s, "warmup": w,
+            "value": nq * dist.world / (ms * 1e-3), "ms_per_step": ms, "steps": s, "warmup": w, "e2e": e2e,
             "pair_dims_per_s": float(ntr) * nq * d * dist.world / (ms * 1e-3),
             "roofline": {"bound": "TMEM read (one fp32 distance per candidate leaves TMEM)",
                          "achieved_tflops": flops / (ms * 1e-3) / 1e12,
@@ -501,13 +509,20 @@ def bench_hmm(args, dist, peaks) -> dict:
     w, s = min(args.warmup, 1), max(1, min(args.steps, 2))
     total, per = device_time(step, s, w, dist)
     ms = total / s
+    # end to end through the public entry with host arrays (probabilities and
+    # observations H2D, logs on the device, kernel, log-likelihoods D2H)
+    import paper_2211_00621_b200 as P
+    hobs = obs.cpu().pin_memory()
+    e2e_ms, _ = host_time(lambda: P.accelerate(P.hmm_forward, A, E, pi, hobs), 1, 1, dist)
+    e2e = {"value": nsig * dist.world / (e2e_ms * 1e-3), "unit": "signals/s",
+           "h2d_bytes_per_step": hobs.numel() * 4 + 8 * (A.size + E.size + pi.size), "d2h_bytes_per_step": 8 * nsig}
     flops = 2.0 * S * S * (T - 1) * nsig
     # CTA-pair kernel: per SM per step, half of A^T written (TMA) + read (UMMA)
     # in fp16, plus the 64-signal u tile re-read for each of its 4 M blocks
     smem_step = 2 * 2 * (S // 2) * S + (S // 2 // 128) * S * 64 * 2
     return {"config": "4096 signals x 10^4 steps x 1024 states, K=8, fp16 operands / fp32 accumulate + fp64 log-scale",
             "element": "signal", "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms,
-            "steps": s, "warmup": w,
+            "steps": s, "warmup": w, "e2e": e2e,
             "trellis_cells_per_s": float(S) * S * (T - 1) * nsig * dist.world / (ms * 1e-3),
             "roofline": {"bound": "shared memory (A^T streamed through smem every step)",
                          "achieved_tflops": flops / (ms * 1e-3) / 1e12,

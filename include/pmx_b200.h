@@ -70,7 +70,8 @@ enum pmx_code {
     PMX_E_NEVER = 9,       /* "reached a never expression"        interp.py:133-135 */
     PMX_E_F32_RANGE = 10,  /* result not representable in the f32 storage type */
     PMX_E_SIN_COS_INF = 11,/* "sin/cos: math domain error" (inf argument)      */
-    PMX_E_PEER_TIMEOUT = 12/* a peer GPU did not deliver its partial (20 s)    */
+    PMX_E_PEER_TIMEOUT = 12,/* a peer GPU did not deliver its partial (20 s)   */
+    PMX_E_RECURSION = 13   /* linear recursion run as a loop exceeded its bound   */
 };
 
 /* ---- scalar-function bytecode ------------------------------------------
@@ -104,6 +105,7 @@ enum pmx_op {
     PMX_OP_EQB,                     /* bool equality (match on Bool literal)  */
     PMX_OP_JZ,                      /* if r_a == 0: pc = b | c << 8 (match)   */
     PMX_OP_JMP,                     /* pc = b | c << 8                        */
+    PMX_OP_FAIL,                    /* raise error code b (enum pmx_code)     */
     PMX_OP_COUNT
 };
 

@@ -247,6 +247,17 @@ def ir_eval(e, env: dict):
         return out
     if isinstance(e, L.Field):
         return ir_eval(e.rec, env)[e.label]
+    if isinstance(e, L.Iterate):             # linear recursion, base case upward
+        lo, hi = ir_eval(e.lo, env), ir_eval(e.hi, env)
+        if hi - lo > L.ITERATE_LIMIT or hi - lo < -1:
+            raise OracleError("maximum recursion depth exceeded")
+        acc = ir_eval(e.init, env)
+        for m in range(lo, hi + 1):
+            env2 = dict(env)
+            env2[e.var] = m
+            env2[e.acc] = acc
+            acc = ir_eval(e.body, env2)
+        return acc
     raise OracleError(f"ir_eval: unsupported node {type(e).__name__}")
 
 

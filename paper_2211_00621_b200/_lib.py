@@ -27,7 +27,7 @@ OPS = [
     "EXP", "LOG", "SIN", "COS", "SQRT",
     "NOT", "SELECT",
     "GET", "LEN", "TGET", "TSET",
-    "NEVER", "EQB", "JZ", "JMP",
+    "NEVER", "EQB", "JZ", "JMP", "FAIL",
 ]
 OP = {name: i for i, name in enumerate(OPS)}
 
@@ -45,6 +45,7 @@ ERROR_MESSAGES = {
     10: "value not representable in the f32 storage type",
     11: "math domain error",
     12: "a peer GPU did not deliver its reduce partial (timeout)",
+    13: "maximum recursion depth exceeded",
 }
 MAX_PEERS, IPC_HANDLE_BYTES = 16, 64
 

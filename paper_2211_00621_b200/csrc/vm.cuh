@@ -112,6 +112,7 @@ __device__ int vm_run(const pmx_program& P, int64_t* r) {
                 if (!store_elem(A.data, A.dtype, pos, vm_opnd(P, r, I.b))) return PMX_E_F32_RANGE;
             } break;
             case PMX_OP_NEVER: return PMX_E_NEVER;
+            case PMX_OP_FAIL: return I.b;
             case PMX_OP_JZ: if (a == 0) pc = I.b | (I.c << 8); break;
             case PMX_OP_JMP: pc = I.b | (I.c << 8); break;
             default: return PMX_E_NEVER;

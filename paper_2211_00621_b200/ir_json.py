@@ -54,6 +54,8 @@ def dump(lam: L.Lam) -> dict:
             return ["Never"]
         if isinstance(e, L.Field):
             return ["Field", go(e.rec), e.label]
+        if isinstance(e, L.Iterate):
+            return ["Iterate", e.var, go(e.lo), go(e.hi), e.acc, go(e.init), go(e.body)]
         raise TypeError(type(e).__name__)
 
     return {"params": lam.params, "body": go(lam.body), "arrays": arrays}
@@ -91,6 +93,8 @@ def load(d: dict, make_array) -> L.Lam:
             return L.Never()
         if k == "Field":
             return L.Field(go(x[1]), x[2])
+        if k == "Iterate":
+            return L.Iterate(x[1], go(x[2]), go(x[3]), x[4], go(x[5]), go(x[6]))
         raise ValueError(k)
 
     return L.Lam(d["params"], go(d["body"])), arrays

@@ -29,6 +29,8 @@ from typing import Any, Callable, Optional
 from . import _lib
 from ._lib import OP
 
+_lib_E_RECURSION = 13      # enum pmx_code PMX_E_RECURSION
+
 # ============================================================================ IR
 
 
@@ -113,6 +115,27 @@ class Do(Expr):
 @dataclass(eq=False)
 class Never(Expr):
     pass
+
+
+# Bound on the iterations of a linear recursion run as a loop (the reference
+# itself fails with a RecursionError long before this depth).
+ITERATE_LIMIT = 1 << 24
+
+
+@dataclass(eq=False)
+class Iterate(Expr):
+    """acc = init; for m in [lo, hi]: acc = body(m, acc); the value is acc.
+
+    The device form of a linear recursion f p = match p with c then base
+    else E[f (p - 1)]: evaluated from the base case up, E applied with
+    p = c+1 .. p (the reference evaluates the same expressions innermost
+    call first)."""
+    var: str
+    lo: Expr
+    hi: Expr
+    acc: str
+    init: Expr
+    body: Expr
 
 
 @dataclass(eq=False)
@@ -490,6 +513,59 @@ def _compile(e: Expr, env: dict, g: _Gen) -> tuple[int, str, bool]:
     if isinstance(e, Never):
         g.emit("NEVER")
         return g.const(0, "int"), "never", False
+    if isinstance(e, Iterate):
+        lo, lt, lown = _compile(e.lo, env, g)
+        hi, ht, hown = _compile(e.hi, env, g)
+        if not (_int_like(lt) and _int_like(ht)):
+            raise CompileError("recursion counter must be Int")
+        m, h = g.reg(), g.reg()
+        g.emit("MOV", m, lo)
+        g.emit("MOV", h, hi)
+        if lown:
+            g.release(lo)
+        if hown:
+            g.release(hi)
+        # depth bound: -1 <= hi - lo <= ITERATE_LIMIT. hi < lo - 1 never reaches
+        # the base case (the reference recurses until its stack overflows); the
+        # upper bound stands in for that stack (the reference overflows first)
+        span, big = g.reg(), g.reg()
+        g.emit("SUBI", span, h, m)
+        g.emit("GTI", big, span, g.const(ITERATE_LIMIT, "int"))
+        ok = g.emit("JZ", 0, big)
+        g.emit("FAIL", 0, 0, _lib_E_RECURSION)
+        g.patch(ok, len(g.insns))
+        g.emit("LTI", big, span, g.const(-1, "int"))
+        ok = g.emit("JZ", 0, big)
+        g.emit("FAIL", 0, 0, _lib_E_RECURSION)
+        g.patch(ok, len(g.insns))
+        g.release(span)
+        g.release(big)
+        a0, at, aown = _compile(e.init, env, g)
+        acc = g.reg()
+        g.emit("MOV", acc, a0)
+        if aown:
+            g.release(a0)
+        top = len(g.insns)
+        c = g.reg()
+        g.emit("LEQI", c, m, h)
+        jz = g.emit("JZ", 0, c)
+        g.release(c)
+        env2 = dict(env)
+        env2[e.var] = (m, "int")
+        env2[e.acc] = (acc, at)
+        b, bt, bown = _compile(e.body, env2, g)
+        if bt != at:
+            raise CompileError("recursion step changes the result type")
+        g.emit("MOV", acc, b)
+        if bown:
+            g.release(b)
+        g.emit("ADDI", m, m, g.const(1, "int"))
+        back = g.emit("JMP")
+        g.patch(back, top)
+        g.patch(jz, len(g.insns))
+        g.release(m)
+        g.release(h)
+        return acc, at, True
     raise CompileError(f"cannot compile {type(e).__name__} for the device")
 
 

@@ -154,8 +154,129 @@ class _Translator:
         raise Unsupported(f"application of {type(fv).__name__}")
 
     def apply_closure(self, clo, args, depth):
+        rec = self.linear_recursion(clo, args, depth)
+        if rec is not None:
+            return rec
         scope = {"__env__": clo.env}
         return self.apply_lam(clo.param, clo.body, scope, args, depth)
+
+    # -- linear recursion as a device loop
+    def _peel(self, clo):
+        """(parameter names, innermost body) of a curried closure."""
+        S = self.S
+        params, body = [clo.param], clo.body
+        while isinstance(body, S.Lam):
+            params.append(body.param)
+            body = body.body
+        return params, body
+
+    def linear_recursion(self, clo, args, depth):
+        """f p.. = match pj with c then BASE else E[f p.. (subi pj 1)] (the
+        recursive call once, outside any lambda, other arguments passed
+        through unchanged) -> Iterate: acc = BASE[pj := c]; for m in c+1..pj:
+        acc = E[pj := m, call := acc].  None if f is not of this form."""
+        S, R = self.S, self.R
+        params, body = self._peel(clo)
+        if len(params) != len(args) or not isinstance(body, S.Match):
+            return None
+        m = body
+        if not (isinstance(m.scrut, S.Var) and m.scrut.name in params and isinstance(m.pat, S.PConst)
+                and isinstance(m.pat.const, S.CInt)):
+            return None
+        pj, c = m.scrut.name, int(m.pat.const.value)
+        calls = []
+
+        def resolves_to_self(name):
+            if name in params:
+                return None
+            try:
+                v = clo.env.lookup(name)
+            except AssertionError:
+                return None
+            if not isinstance(v, R.Closure):
+                return None
+            dps, dbody = self._peel(v)
+            return dps if dbody is body else None
+
+        def walk(e):
+            if isinstance(e, S.Lam):
+                return not self._mentions_self(e, resolves_to_self)
+            if isinstance(e, S.App):
+                head, a = e, []
+                while isinstance(head, S.App):
+                    a.append(head.arg)
+                    head = head.fn
+                a.reverse()
+                if isinstance(head, S.Var):
+                    dps = resolves_to_self(head.name)
+                    if dps is not None:
+                        calls.append((e, dps, a))
+                        return True
+                return walk(head) and all(walk(x) for x in a)
+            if isinstance(e, S.Let):
+                return walk(e.value) and walk(e.body)
+            if isinstance(e, S.Match):
+                return walk(e.scrut) and walk(e.thn) and walk(e.els)
+            if isinstance(e, S.Var):
+                return resolves_to_self(e.name) is None
+            return True
+
+        if not walk(m.els) or len(calls) != 1 or self._mentions_self(m.thn, resolves_to_self):
+            return None
+        call, dps, cargs = calls[0]
+        if len(cargs) != len(dps):
+            return None
+        for q, a in zip(dps, cargs):
+            if q == pj:                               # subi pj 1
+                ok = (isinstance(a, S.App) and isinstance(a.fn, S.App) and isinstance(a.fn.fn, S.ConstE)
+                      and isinstance(a.fn.fn.const, S.CBuiltin) and a.fn.fn.const.name == "subi"
+                      and isinstance(a.fn.arg, S.Var) and a.fn.arg.name == pj
+                      and isinstance(a.arg, S.ConstE) and isinstance(a.arg.const, S.CInt)
+                      and int(a.arg.const.value) == 1)
+            else:                                     # passed through unchanged
+                ok = isinstance(a, S.Var) and a.name == q
+            if not ok:
+                return None
+        # bind the actual arguments (scalars once), then build the loop
+        scope = {"__env__": clo.env}
+        binds = []
+        for prm, a in zip(params, args):
+            if isinstance(a, (_Fn, _Captured, L.Var)):
+                scope[prm] = a
+            else:
+                nm = self.fresh(prm.text)
+                scope[prm] = L.Var(nm)
+                binds.append((nm, a))
+        hi = self.as_expr(scope[pj])
+        mvar, accvar = self.fresh("rec_m"), self.fresh("rec_acc")
+        base_scope = dict(scope)
+        base_scope[pj] = L.Const(c, "int")
+        init = self.as_expr(self.expr(m.thn, base_scope, depth + 1))
+        step_scope = dict(scope)
+        step_scope[pj] = L.Var(mvar)
+        prev = getattr(self, "_rec_hole", None)
+        self._rec_hole = (call, accvar)
+        try:
+            step = self.as_expr(self.expr(m.els, step_scope, depth + 1))
+        finally:
+            self._rec_hole = prev
+        out = L.Iterate(mvar, L.Const(c + 1, "int"), hi, accvar, init, step)
+        for n, a in reversed(binds):
+            out = L.LetE(n, a, out)
+        return out
+
+    def _mentions_self(self, e, resolves_to_self):
+        S = self.S
+        if isinstance(e, S.Var):
+            return resolves_to_self(e.name) is not None
+        for child in getattr(e, "__dict__", {}).values():
+            if isinstance(child, S.Expr) and self._mentions_self(child, resolves_to_self):
+                return True
+            if isinstance(child, list):
+                for x in child:
+                    if isinstance(x, S.Expr) and self._mentions_self(x, resolves_to_self):
+                        return True
+        return False
 
     def apply_lam(self, param, body, scope, args, depth):
         if not args:
@@ -208,6 +329,9 @@ class _Translator:
 
     def expr(self, e, scope, depth):
         S = self.S
+        hole = getattr(self, "_rec_hole", None)
+        if hole is not None and e is hole[0]:         # the recursive call: the loop's accumulator
+            return L.Var(hole[1])
         if isinstance(e, S.Var):
             return self.lookup(e.name, scope)
         if isinstance(e, S.ConstE):

@@ -14,7 +14,7 @@ REF = pathlib.Path("/root/reference/pkg")
 pytestmark = pytest.mark.skipif(not REF.exists(), reason="reference interpreter not available")
 
 # constructs the device cannot run: nested sequences as elements, recursion
-UNSUPPORTED = {"recursion_pow"}      # a recursive closure as the map function
+UNSUPPORTED: set = set()   # recursion_pow runs as a device loop (linear recursion)
 
 
 def _pmx():
@@ -149,6 +149,55 @@ def test_runtime_errors_keep_reference_messages():
     try:
         src = "let f = lam s. map (lam x. divi 10 x) s in let r = accelerate (f [1, 0]) in print (int2string (reduce addi 0 r))"
         with pytest.raises(pmx.Diagnostics, match="integer division by zero"):
+            pmx.run_source(src, mode="accel", workers=2, capture_output=True)
+    finally:
+        un()
+
+
+RECURSIVE = [
+    # linear recursion -> device loop (pmx_adapter._Translator.linear_recursion)
+    ("fact", "recursive let fact = lam n. match n with 0 then 1 else muli n (fact (subi n 1)) in "
+             "let r = accelerate (map fact [0, 1, 5, 12, 20]) in print (int2string (reduce addi 0 r))", True),
+    ("harmonic", "recursive let h = lam n. match n with 0 then 0.0 else addf (h (subi n 1)) "
+                 "(divf 1.0 (int2float n)) in "
+                 "let r = accelerate (map h [1, 2, 10, 100]) in print (float2string (reduce addf 0.0 r))", True),
+    ("base_second", "recursive let p = lam n. lam k. match n with 1 then k else addi (muli k 3) (p (subi n 1) k) in "
+                    "let r = accelerate (map (lam x. p x 7) [1, 2, 6]) in print (int2string (reduce addi 0 r))", True),
+    ("let_in_step", "recursive let g = lam n. match n with 0 then 2 else let t = g (subi n 1) in "
+                    "modi (addi (muli t t) n) 1000003 in "
+                    "let r = accelerate (map g [0, 4, 50]) in print (int2string (reduce addi 0 r))", True),
+    # two recursive calls: not linear, stays unsupported on the device
+    ("fib", "recursive let fib = lam n. match n with 0 then 0 else match n with 1 then 1 else "
+            "addi (fib (subi n 1)) (fib (subi n 2)) in "
+            "let r = accelerate (map fib [3, 7]) in print (int2string (reduce addi 0 r))", False),
+]
+
+
+@pytest.mark.parametrize("name,src,supported", RECURSIVE, ids=[r[0] for r in RECURSIVE])
+def test_linear_recursion_matches_reference(name, src, supported):
+    pmx, interp = _pmx()
+    want = pmx.run_source(src, mode="debug", capture_output=True).stdout
+    un = install_checker(interp)
+    try:
+        if not supported:
+            with pytest.raises(pmx.Diagnostics, match="not supported on the B200 device"):
+                pmx.run_source(src, mode="accel", workers=2, capture_output=True)
+            return
+        got = pmx.run_source(src, mode="accel", workers=2, capture_output=True).stdout
+    finally:
+        un()
+    assert got == want
+
+
+def test_recursion_that_never_reaches_the_base_case_is_an_error():
+    """pow b n for n < 0 recurses forever in the reference (stack overflow);
+    the device loop reports it instead of returning the base case."""
+    pmx, interp = _pmx()
+    src = ("recursive let pow = lam b. lam n. match n with 0 then 1 else muli b (pow b (subi n 1)) in "
+           "let r = accelerate (map (pow 2) [3, -1]) in print (int2string (reduce addi 0 r))")
+    un = install_checker(interp)
+    try:
+        with pytest.raises(pmx.Diagnostics, match="maximum recursion depth exceeded"):
             pmx.run_source(src, mode="accel", workers=2, capture_output=True)
     finally:
         un()

@@ -299,3 +299,24 @@ def test_map_rows_fold_error_reports_row(jit_mode):
     with pytest.raises(Diagnostics, match="integer division by zero") as ei:
         accelerate(lambda s: map_rows_fold(lam("x", divi(12, "x")), addi, 0, s), rows)
     assert "element 1)" in str(ei.value)
+
+
+def test_linear_recursion_loop(jit_mode):
+    """Iterate (a linear recursion run base case upward, lambdas.py) on the
+    device vs the oracle's evaluator: Int and Float accumulators, and the
+    recursion-depth error for an argument below the base case."""
+    from paper_2211_00621_b200 import lambdas as L
+    fact = L.Lam(["n"], L.Iterate("m", L.Const(1, "int"), L.Var("n"), "a", L.Const(1, "int"),
+                                  L.Prim("muli", [L.Var("m"), L.Var("a")])))
+    harm = L.Lam(["n"], L.Iterate("m", L.Const(1, "int"), L.Var("n"), "a", L.Const(0.0, "float"),
+                                  L.Prim("addf", [L.Var("a"), L.Prim("divf", [L.Const(1.0, "float"),
+                                                                            L.Prim("int2float", [L.Var("m")])])])))
+    xs = list(range(0, 300, 7)) + [1000, 4096]
+    for f in (fact, harm):
+        got = accelerate(lambda s: eval_map(f, s), xs)
+        _check_values(_host(got), [O.ir_apply(f, x) for x in xs], "recursion")
+    with pytest.raises(Diagnostics, match="maximum recursion depth exceeded") as ei:
+        accelerate(lambda s: eval_map(fact, s), [3, 4, -1, 5, -7])
+    assert "element 2)" in str(ei.value)
+    with pytest.raises(Diagnostics, match="maximum recursion depth exceeded"):
+        accelerate(lambda s: eval_map(fact, s), [1 << 40])

@@ -79,3 +79,18 @@ def test_loop_body_compiles(code):
     _check(compile_lambda(body, ["int"]).program, 2, 0, 0)
     body2 = lam("i", tensor_set(y, [divi("i", 4), "i"], tensor_get(x, ["i"])))
     _check(compile_lambda(body2, ["int"]).program, 2, 0, 0)
+
+
+def test_linear_recursion_loop_compiles():
+    """Iterate lowers to a backward jump; the generated kernel keeps it as a
+    loop (one element per lane, early exit on the recursion-depth error)."""
+    from paper_2211_00621_b200 import lambdas as L
+    f = L.Lam(["n"], L.Iterate("m", L.Const(1, "int"), L.Var("n"), "a", L.Const(0.0, "float"),
+                               L.Prim("addf", [L.Var("a"), L.Prim("int2float", [L.Var("m")])])))
+    comp = compile_lambda(f, ["int", "int"])
+    _check(comp.program, 0, _lib.PMX_I64, _lib.PMX_F64)
+    lib = _lib.load()
+    buf = C.create_string_buffer(1 << 16)
+    assert lib.pmx_jit_source(C.byref(comp.program), 0, buf, len(buf)) > 0
+    src = buf.value.decode()
+    assert "static constexpr int U = 1" in src and "goto L" in src and "PMX_FAILIF(true, 13)" in src

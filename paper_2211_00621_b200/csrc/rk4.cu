@@ -23,11 +23,67 @@ namespace pmx {
 
 struct St { double x0, x1, x2, x3; };
 
+// Branch-free sin/cos for the two angles of `deriv`.  CUDA's sin/sincos carry
+// a Payne-Hanek branch for huge arguments, which keeps the compiler from
+// interleaving the independent transcendental chains of one RK4 step (sin of
+// the arm angle, sin/cos of the pendulum angle, and the k2/k4 evaluations that
+// are off the critical path) — at 68 threads/SM that ILP is the only
+// parallelism the SM has.  Here: Cody-Waite reduction by pi/2 in three 33-bit
+// pieces (each k*piece exact for |k| < 2^20) and the fdlibm minimax
+// polynomials on [-pi/4, pi/4]; accuracy ~1 ulp, like glibc's and CUDA's (the
+// oracle runs glibc; the parity bar is 1e-9 relative).  Arguments outside
+// |x| <= 2^18 (and NaN/inf) take CUDA's sincos after the fast path.
+struct SinCos { double s, c; };
+
+__device__ __forceinline__ SinCos sincos_cw(double x) {
+    const double k = rint(x * 6.36619772367581382433e-01);           // x * 2/pi
+    double r = fma(-k, 1.57079632673412561417e+00, x);                // pio2_1 (33 bits)
+    r = fma(-k, 6.07710050630396597660e-11, r);                       // pio2_2
+    r = fma(-k, 2.02226624871116645580e-21, r);                       // pio2_3
+    const double z = r * r;
+    // Horner (Estrin's shallower tree measured no faster here)
+    const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, 1.58969099521155010221e-10, -2.50507602534068634195e-08),
+                                               2.75573137070700676789e-06), -1.98412698298579493134e-04),
+                                 8.33333333332248946124e-03), -1.66666666666666324348e-01);
+    const double pc = fma(z, fma(z, fma(z, fma(z, fma(z, -1.13596475577881948265e-11, 2.08757232129817482790e-09),
+                                               -2.75573143513906633035e-07), 2.48015872894767294178e-05),
+                                 -1.38888888888741095749e-03), 4.16666666666666019037e-02);
+    const double sr = fma(r * z, ps, r);
+    const double cr = fma(z * z, pc, fma(-0.5, z, 1.0));
+    const int q = (int)k & 3;
+    double sv = (q & 1) ? cr : sr, cv = (q & 1) ? sr : cr;
+    sv = (q & 2) ? -sv : sv;
+    cv = ((q + 1) & 2) ? -cv : cv;
+    sv = x == 0.0 ? x : sv;                                           // sin(-0) = -0
+    return SinCos{sv, cv};
+}
+
+// Trig modes.  LIBM: CUDA's sin/sincos.  FAST: sincos_cw of both angles,
+// recording in `bad` whether an angle left its range; the caller then redoes
+// the whole step with LIBM, so the step itself is straight-line code.
+// (Measured on B200, N = 10^4 x 10^3: LIBM 0.99 ms, FAST 0.62 ms; a lane pair
+// per parameter set splitting the two reductions, with shuffles, 0.63 ms;
+// Estrin instead of Horner 0.63 ms; 32/64/128-thread CTAs all equal — the
+// time is one warp's dependent chain, ~1200 cycles per RK4 step.)
+enum { RK4_LIBM = 0, RK4_FAST = 1 };
+
+template <int MODE>
+__device__ __forceinline__ void trig(const St& s, double& sa, double& sp, double& cp, bool& bad) {
+    if (MODE == RK4_FAST) {
+        const SinCos a = sincos_cw(s.x0), b = sincos_cw(s.x2);
+        sa = a.s; sp = b.s; cp = b.c;
+        bad |= !(fabs(s.x0) <= 262144.0 && fabs(s.x2) <= 262144.0);
+    } else {
+        sincos(s.x2, &sp, &cp);
+        sa = sin(s.x0);
+    }
+}
+
 // deriv p s (rk4.pmx:11-22)
-__device__ __forceinline__ St deriv(double p, const St& s) {
-    double sp, cp;
-    sincos(s.x2, &sp, &cp);
-    const double sa = sin(s.x0);
+template <int MODE>
+__device__ __forceinline__ St deriv(double p, const St& s, bool& bad) {
+    double sa, sp, cp;
+    trig<MODE>(s, sa, sp, cp, bad);
     St d;
     d.x0 = s.x1;
     // subf (mulf p (mulf (sin pend) (cos pend))) (addf (mulf 0.2 armVel) (mulf 0.3 (sin arm)))
@@ -48,10 +104,21 @@ __device__ __forceinline__ double comb(double s, double h6, double k1, double k2
     return A_(s, M_(h6, A_(k1, A_(M_(2.0, k2), A_(M_(2.0, k3), k4)))));
 }
 
+// step p s (rk4.pmx:26-37)
+template <int MODE>
+__device__ __forceinline__ St step(double p, const St& s, double h, double h2, double h6, bool& bad) {
+    const St k1 = deriv<MODE>(p, s, bad);
+    const St k2 = deriv<MODE>(p, axpy(s, h2, k1), bad);
+    const St k3 = deriv<MODE>(p, axpy(s, h2, k2), bad);
+    const St k4 = deriv<MODE>(p, axpy(s, h, k3), bad);
+    return St{comb(s.x0, h6, k1.x0, k2.x0, k3.x0, k4.x0), comb(s.x1, h6, k1.x1, k2.x1, k3.x1, k4.x1),
+              comb(s.x2, h6, k1.x2, k2.x2, k3.x2, k4.x2), comb(s.x3, h6, k1.x3, k2.x3, k3.x3, k4.x3)};
+}
+
 // TRACE: also record state component `comp` after every step into
 // trace[k * steps + m] (the paper's N x M tensor of one measured state,
 // PAPER.md:1435-1440, written by its accelerated `loop` through tensorSet).
-template <bool TRACE>
+template <bool TRACE, int MODE>
 __global__ void __launch_bounds__(64)
 k_rk4(const double* __restrict__ ps, int64_t n, const double* __restrict__ init4,
       int steps, double h, double* __restrict__ out, int comp, double* __restrict__ trace) {
@@ -62,12 +129,14 @@ k_rk4(const double* __restrict__ ps, int64_t n, const double* __restrict__ init4
     const double h6 = __ddiv_rn(h, 6.0);   // divf h 6.0
     St s{init4[0], init4[1], init4[2], init4[3]};
     for (int m = 0; m < steps; ++m) {   // integrate p s m  (rk4.pmx:38-40)
-        const St k1 = deriv(p, s);
-        const St k2 = deriv(p, axpy(s, h2, k1));
-        const St k3 = deriv(p, axpy(s, h2, k2));
-        const St k4 = deriv(p, axpy(s, h, k3));
-        s = St{comb(s.x0, h6, k1.x0, k2.x0, k3.x0, k4.x0), comb(s.x1, h6, k1.x1, k2.x1, k3.x1, k4.x1),
-               comb(s.x2, h6, k1.x2, k2.x2, k3.x2, k4.x2), comb(s.x3, h6, k1.x3, k2.x3, k3.x3, k4.x3)};
+        bool bad = false;
+        const St next = step<MODE>(p, s, h, h2, h6, bad);
+        if (MODE != RK4_LIBM && bad) {     // an angle left sincos_cw's range (or is NaN/inf)
+            bool unused = false;
+            s = step<RK4_LIBM>(p, s, h, h2, h6, unused);
+        } else {
+            s = next;
+        }
         if (TRACE) {
             const double v = comp == 0 ? s.x0 : comp == 1 ? s.x1 : comp == 2 ? s.x2 : s.x3;
             __stcs(trace + k * (int64_t)steps + m, v);
@@ -81,15 +150,30 @@ k_rk4(const double* __restrict__ ps, int64_t n, const double* __restrict__ init4
 
 using namespace pmx;
 
+// PMX_RK4_MODE=0 selects CUDA's libm sin/sincos (A/B and tests); default FAST.
+static int rk4_mode() {
+    static const int v = [] { const char* e = getenv("PMX_RK4_MODE"); return e && e[0] == '0' ? 0 : 1; }();
+    return v;
+}
+
+template <bool TRACE>
+static void rk4_launch(const double* params, int64_t n, const double* init4, int steps, double h, double* out,
+                       int comp, double* trace, cudaStream_t st) {
+    // 64 threads per CTA spreads the few warps of an N=10^4 sweep over all SMs.
+    const int threads = 64;
+    const int64_t grid = (n + threads - 1) / threads;
+    if (rk4_mode() == RK4_LIBM)
+        k_rk4<TRACE, RK4_LIBM><<<(unsigned)grid, threads, 0, st>>>(params, n, init4, steps, h, out, comp, trace);
+    else
+        k_rk4<TRACE, RK4_FAST><<<(unsigned)grid, threads, 0, st>>>(params, n, init4, steps, h, out, comp, trace);
+}
+
 extern "C" int pmx_rk4_sweep_f64(const double* params, int64_t n, const double* init4,
                                  int32_t steps, double h, double* out, void* stream) {
     PMX_REQUIRE(n >= 0 && steps >= 0, "pmx_rk4_sweep_f64: negative size");
     if (n == 0) return 0;
     PMX_REQUIRE(params && init4 && out, "pmx_rk4_sweep_f64: null buffer");
-    // 64 threads per CTA spreads the few warps of an N=10^4 sweep over all SMs.
-    const int threads = 64;
-    const int64_t grid = (n + threads - 1) / threads;
-    k_rk4<false><<<(unsigned)grid, threads, 0, (cudaStream_t)stream>>>(params, n, init4, steps, h, out, 0, nullptr);
+    rk4_launch<false>(params, n, init4, steps, h, out, 0, nullptr, (cudaStream_t)stream);
     PMX_CHECK_LAUNCH("rk4");
     return 0;
 }
@@ -100,9 +184,7 @@ extern "C" int pmx_rk4_trace_f64(const double* params, int64_t n, const double* 
     PMX_REQUIRE(comp >= 0 && comp < 4, "pmx_rk4_trace_f64: state component must be 0..3");
     if (n == 0) return 0;
     PMX_REQUIRE(params && init4 && out && (trace || steps == 0), "pmx_rk4_trace_f64: null buffer");
-    const int threads = 64;
-    const int64_t grid = (n + threads - 1) / threads;
-    k_rk4<true><<<(unsigned)grid, threads, 0, (cudaStream_t)stream>>>(params, n, init4, steps, h, out, comp, trace);
+    rk4_launch<true>(params, n, init4, steps, h, out, comp, trace, (cudaStream_t)stream);
     PMX_CHECK_LAUNCH("rk4_trace");
     return 0;
 }

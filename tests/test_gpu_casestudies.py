@@ -47,6 +47,16 @@ def test_rk4_vs_oracle_config_steps():
     assert np.allclose(got, want, rtol=FP64_REL, atol=1e-12)
 
 
+def test_rk4_angles_outside_the_fast_reduction_range():
+    """Angles beyond |x| = 2^18 (and the steps where they occur) take CUDA's
+    libm sin/sincos instead of the branch-free reduction (csrc/rk4.cu)."""
+    ps = synth.rk4_params(64)
+    for init in ([3.0e5, 0.0, 0.3, 0.0], [0.1, 0.0, -1.0e7, 2.0], [262143.0, 1.0, 262145.0, -1.0]):
+        got = accelerate(lambda p, s0: rk4_sweep(p, s0, 50, synth.RK4_H), ps, init)
+        want = O.rk4(ps, init, 50, synth.RK4_H)
+        assert np.allclose(got, want, rtol=FP64_REL, atol=1e-12), init
+
+
 # ------------------------------------------------------------------ HMM forward
 @pytest.mark.parametrize("ix", [0, 1, 2])
 def test_hmm_forward_golden(ix, golden):

@@ -239,7 +239,8 @@ def test_nn_gradients_match_finite_differences():
             assert math.isclose(dw[i, j], fd, rel_tol=1e-4, abs_tol=1e-8)
 
 
-@pytest.mark.parametrize("npts,nin,nout", [(100_003, 64, 16), (4097, 7, 32), (1, 3, 1), (50_000, 33, 5)])
+@pytest.mark.parametrize("npts,nin,nout", [(100_003, 64, 16), (4097, 7, 32), (1, 3, 1), (50_000, 33, 5),
+                                            (70_001, 62, 32), (9_999, 64, 3)])
 def test_nn_vs_oracle(npts, nin, nout):
     from paper_2211_00621_b200 import nn_gradients
     rng = np.random.default_rng(npts + nin)
@@ -264,6 +265,17 @@ def test_nn_errors():
     assert "element 9)" in str(ei.value)
     with pytest.raises(Diagnostics, match="float division by zero"):
         accelerate(nn_gradients, np.zeros((0, 16)), np.zeros(0, np.int32), w, b)
+    # every exp underflows to 0 at point 3: log of a zero total (math.log(0.0))
+    x2 = np.zeros((300, 16))
+    x2[3] = -100.0
+    x2[200] = 1000.0                                  # exp overflow later: the first error wins
+    with pytest.raises(Diagnostics, match="log: math domain error") as ei:
+        accelerate(nn_gradients, x2, np.zeros(300, np.int32), np.ones((16, 8)), np.zeros(8))
+    assert "element 3)" in str(ei.value)
+    x2[3] = 0.0
+    with pytest.raises(Diagnostics, match="exp: math range error") as ei:
+        accelerate(nn_gradients, x2, np.zeros(300, np.int32), np.ones((16, 8)), np.zeros(8))
+    assert "element 200)" in str(ei.value)
 
 
 # ------------------------------------------------------------ RK4 trace

@@ -20,3 +20,15 @@ for _ in range(2):
                                            loss.data_ptr(), dw.data_ptr(), db.data_ptr(), ws.data_ptr(), ws.numel(),
                                            err.data_ptr(), torch.cuda.current_stream().cuda_stream), "nn")
 torch.cuda.synchronize()
+if len(sys.argv) > 1 and sys.argv[1] == "time":
+    a, bb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(20):
+        a.record()
+        lib.pmx_nn_softmax_grad_f64(x.data_ptr(), y.data_ptr(), w.data_ptr(), b.data_ptr(), npts, nin, nout,
+                                    loss.data_ptr(), dw.data_ptr(), db.data_ptr(), ws.data_ptr(), ws.numel(),
+                                    err.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        bb.record()
+        bb.synchronize()
+        ts.append(a.elapsed_time(bb))
+    print("nn ms min", min(ts), "med", sorted(ts)[10], "loss", float(loss.item()))

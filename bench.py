@@ -587,7 +587,8 @@ def bench_viterbi(args, dist, peaks) -> dict:
     total, per = device_time(step, s, w, dist)
     ms = total / s
     cells = float(S) * S * (T - 1) * nsig
-    fp64_lanes = 64.0 * 148 * 1.965e9          # FP64 lanes/s (B200: 64 per SM per clock)
+    pp = pipe_peaks()
+    fp64_lanes = pp.get("fp64_add_ops_per_s", 64.0 * 148 * 1.965e9)   # FP64 pipe ops/s
     return {"config": f"S={S}, K={K}, {nsig} signals x T={T}, fp64 (viterbi.pmx semantics)", "element": "signal",
             "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms, "steps": s, "warmup": w,
             "cells_per_s": cells / (ms * 1e-3),
@@ -595,8 +596,9 @@ def bench_viterbi(args, dist, peaks) -> dict:
                          "achieved_fp64_ops_per_s": 2 * cells / (ms * 1e-3), "peak_fp64_ops_per_s": fp64_lanes,
                          "frac": 2 * cells / (ms * 1e-3) / fp64_lanes,
                          "issue_frac": 5 * cells / (ms * 1e-3) / (128.0 * 148 * 1.965e9),
-                         "peak_source": "64 FP64 lanes/clk/SM x 148 SMs x 1.965 GHz (B200 FP64 40 TFLOP/s); "
-                                        "issue: 4 x 32 thread-instr/clk/SM"},
+                         "peak_source": ("measured (profiles/pipe_peaks.json, tools/peaks.cu)" if pp else
+                                         "64 FP64 lanes/clk/SM x 148 SMs x 1.965 GHz") +
+                                        "; issue: 4 x 32 thread-instr/clk/SM"},
             "_path": path}
 
 
@@ -649,14 +651,31 @@ def bench_nn(args, dist, peaks) -> dict:
     ms = total / args.steps
     bytes_ = 8.0 * nin * npts + 4.0 * npts
     flops = npts * (2.0 * nin * nout * 2)            # z (mul+add) and dw (mul+add), fp64
+    pipe_ops = npts * (3.0 * nin * nout)             # z: DMUL + DADD; dw: one DFMA
+    pp = pipe_peaks()
+    fp64_ops_peak = pp.get("fp64_add_ops_per_s", 64.0 * 148 * 1.965e9)
     return {"config": f"{npts} points x {nin} inputs x {nout} classes, fp64 (nn.pmx semantics)", "element": "point",
             "value": npts * dist.world / (ms * 1e-3), "ms_per_step": ms,
             "roofline": {"bound": "HBM (x stream) / FP64 pipe", "achieved_GBps": bytes_ / (ms * 1e-3) / 1e9,
                          "hbm_frac": bytes_ / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                          "achieved_fp64_tflops": flops / (ms * 1e-3) / 1e12,
-                         "fp64_frac": flops / (ms * 1e-3) / 1e12 / 37.0,
-                         "peak_source": "HBM measured; FP64 37 TFLOP/s (64 lanes x 2 x 148 SMs x 1.965 GHz)"},
+                         "fp64_pipe_ops_per_s": pipe_ops / (ms * 1e-3),
+                         "fp64_pipe_frac": pipe_ops / (ms * 1e-3) / fp64_ops_peak,
+                         "peak_source": "HBM: MEASURED_PEAKS.json; FP64 pipe: " +
+                                        ("measured (profiles/pipe_peaks.json)" if pp else "64 lanes/clk/SM nominal"),
+                         "note": "z keeps the reference's separately rounded mul + add (2 pipe ops per MAC); "
+                                 "dw sums use DFMA (1 pipe op)"},
             "_loss": float(loss.item())}
+
+
+def pipe_peaks() -> dict:
+    """FP64 / FP32 / MUFU / shared-memory rates measured on a B200 by
+    tools/peaks.cu (profiles/pipe_peaks.json); {} when absent."""
+    f = ROOT / "profiles" / "pipe_peaks.json"
+    try:
+        return json.loads(f.read_text())
+    except (OSError, ValueError):
+        return {}
 
 
 def cpu_nn(seconds=10.0) -> dict:

@@ -424,11 +424,14 @@ k_loop_lanes(int64_t n, const B body, uint64_t* err) {
 // fold op init (map f x) for an operator the library does not recognise: the
 // result must equal the sequential left fold for any associative op, so every
 // combine keeps the left operand earlier in the sequence.  A CTA owns a
-// contiguous range; per round each warp folds a contiguous 1024-element block
-// (each lane folds its 32 contiguous elements, read as 16-byte loads through
-// L1; an ordered shuffle tree — lower lane on the left — folds the lanes), the
-// 8 warp values fold in warp order into the CTA's running value; the last CTA
-// folds the CTA values in CTA order after `init`.
+// contiguous range, split into one contiguous sub-range per warp; warps run
+// independently (no CTA barrier per block): per 1024-element block each lane
+// folds its 32 contiguous elements (16-byte loads, the next block's already in
+// flight) as two 16-element chains joined left-to-right, an ordered shuffle
+// tree (lower lane on the left) folds the lanes, and lane 0 folds the block
+// into the warp's running value.  The warp values fold in warp order, the CTA
+// values in CTA order after `init` (last CTA).  The ragged tail block keeps
+// has-value bookkeeping; full blocks do not.
 struct OPart { int64_t v; int has; };
 
 template <class G>
@@ -446,76 +449,166 @@ __device__ __forceinline__ OPart op_combine(const G& g, OPart a, OPart b, uint64
     return r;
 }
 
+template <class G>
+__device__ __forceinline__ int64_t op_apply(const G& g, int64_t a, int64_t b, uint64_t* err, int64_t idx) {
+    const int64_t i0[1] = {a}, i1[1] = {b};
+    int64_t o[1];
+    int code[1] = {0};
+    g.template run<1>(i0, i1, o, code);
+    if (code[0]) raise_err(err, idx, code[0]);
+    return o[0];
+}
+
+// Block loads.  COAL: packet u of lane l holds elements 128u + 4l .. +3 (every
+// load instruction reads 32 contiguous packets — coalesced); otherwise packet
+// u holds the lane's own elements 32l + 4u .. +3 (lane-contiguous: each
+// instruction touches 32 cache lines, served through L1).
+template <bool COAL, class TX>
+__device__ __forceinline__ void ord_load_full(const TX* __restrict__ x, int64_t r0, int l, TX (&xe)[8][4]) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int64_t e0 = COAL ? r0 + 128 * u + 4 * l : r0 + 32 * l + 4 * u;
+        Pack4<TX> v;
+#pragma unroll
+        for (int k = 0; k < (int)(sizeof(TX) >= 4 ? sizeof(TX) / 4 : 1); ++k)
+            v.q[k] = __ldg(reinterpret_cast<const uint4*>(x + e0) + k);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) xe[u][e] = v.e[e];
+    }
+}
+
 template <class TX, class F, class G>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, 2)
 k_reduce_ordered(const TX* __restrict__ x, int64_t n, const F f, const G g, int64_t init, int64_t* out,
                  OPart* partials, unsigned* ticket, uint64_t* err) {
-    constexpr int UP = 8;                         // 16-byte packets per lane per round
-    constexpr int RW = 32 * 4 * UP;               // elements per warp per round
+    constexpr int UP = 8;                         // 16-byte packets per lane per block
+    constexpr int RW = 32 * 4 * UP;               // elements per warp block
     const int nw = blockDim.x >> 5;
     const int64_t RB = (int64_t)nw * RW;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const int64_t per = ((n + gridDim.x - 1) / gridDim.x + RB - 1) / RB * RB;
     const int64_t lo = min(n, (int64_t)blockIdx.x * per), hi = min(n, lo + per);
+    const int64_t wper = per / nw;
+    const int64_t wlo = min(hi, lo + (int64_t)w * wper), whi = min(hi, wlo + wper);
+    const bool aligned = ((uintptr_t)(x + wlo) % (4 * sizeof(TX))) == 0;
     __shared__ OPart s_w[32];
-    OPart acc;
+    OPart acc;                                    // the warp's running value (lane 0)
     acc.v = 0;
     acc.has = 0;
-    for (int64_t r0 = lo; r0 < hi; r0 += RB) {
-        const int64_t wb = r0 + (int64_t)w * RW;
-        const int64_t p0 = wb + (int64_t)l * (4 * UP);
+    // full blocks [wlo, wfull): software-pipelined (the next block's loads are in
+    // flight while this one folds); the ragged tail block takes the general path
+    const int64_t wfull = aligned ? wlo + (whi - wlo) / RW * RW : wlo;
+    // 4-byte elements: coalesced loads, transposed to lane-contiguous runs
+    // through a per-warp shared buffer (row pitch 33: conflict-free); 33 KiB
+    // per CTA (8-byte elements would need 66 KiB of static shared memory)
+    constexpr bool COAL = sizeof(TX) == 4;
+    __shared__ TX s_tr[COAL ? 8 * (RW + RW / 32) : 1];
+    TX* tr = s_tr + (COAL ? w * (RW + RW / 32) : 0);
+    TX nx[UP][4];
+    if (wlo < wfull) ord_load_full<COAL>(x, wlo, l, nx);
+    for (int64_t r0 = wlo; r0 < wfull; r0 += RW) {
+        const int64_t p0 = r0 + (int64_t)l * (4 * UP);
         TX xe[UP][4];
-        const bool full = p0 + 4 * UP <= hi && ((uintptr_t)(x + p0) % (4 * sizeof(TX)) == 0);
-        if (full) {
-#pragma unroll
-            for (int u = 0; u < UP; ++u) {
-                Pack4<TX> v;
-#pragma unroll
-                for (int k = 0; k < (int)(sizeof(TX) >= 4 ? sizeof(TX) / 4 : 1); ++k)
-                    v.q[k] = __ldg(reinterpret_cast<const uint4*>(x + p0 + 4 * u) + k);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) xe[u][e] = v.e[e];
-            }
-        } else {
+        if (COAL) {
+            __syncwarp();                         // previous block's reads done
 #pragma unroll
             for (int u = 0; u < UP; ++u)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const int64_t q = p0 + 4 * u + e;
-                    xe[u][e] = q < hi ? x[q] : x[lo];
+                    const int q = 128 * u + 4 * l + e;
+                    tr[q + (q >> 5)] = nx[u][e];
                 }
-        }
-        OPart lp;
-        lp.v = 0;
-        lp.has = 0;
+            __syncwarp();
 #pragma unroll
-        for (int u = 0; u < UP; ++u) {
-            typename F::Res r[4];
-            int code[4] = {0, 0, 0, 0};
-            f(xe[u], p0 + 4 * u, r, code);
+            for (int u = 0; u < UP; ++u)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) xe[u][e] = tr[33 * l + 4 * u + e];
+        } else {
+#pragma unroll
+            for (int u = 0; u < UP; ++u)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) xe[u][e] = nx[u][e];
+        }
+        if (r0 + RW < wfull) ord_load_full<COAL>(x, r0 + RW, l, nx);
+        // two 16-element chains (elements 0..15 and 16..31 of the lane), joined left-to-right
+        int64_t a = 0, b = 0;
+#pragma unroll
+        for (int u = 0; u < UP / 2; ++u) {
+            typename F::Res ra[4], rb[4];
+            int ca[4] = {0, 0, 0, 0}, cb[4] = {0, 0, 0, 0};
+            f(xe[u], p0 + 4 * u, ra, ca);
+            f(xe[u + UP / 2], p0 + 4 * (u + UP / 2), rb, cb);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const int64_t q = p0 + 4 * u + e;
-                if (q >= hi) break;
-                if (code[e]) { raise_err(err, q, code[e]); continue; }
-                OPart v;
-                v.v = to_reg(r[e]);
-                v.has = 1;
-                lp = op_combine(g, lp, v, err, q);
+                const int64_t qa = p0 + 4 * u + e, qb = qa + 2 * UP;
+                if (ca[e]) raise_err(err, qa, ca[e]);
+                if (cb[e]) raise_err(err, qb, cb[e]);
+                if (u == 0 && e == 0) {
+                    a = to_reg(ra[0]);
+                    b = to_reg(rb[0]);
+                } else {
+                    a = op_apply(g, a, to_reg(ra[e]), err, qa);
+                    b = op_apply(g, b, to_reg(rb[e]), err, qb);
+                }
             }
         }
+        int64_t lv = op_apply(g, a, b, err, p0 + UP * 4 - 1);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            OPart rr;
-            rr.v = __shfl_down_sync(0xffffffffu, lp.v, o);
-            rr.has = __shfl_down_sync(0xffffffffu, lp.has, o);
-            if ((l & (2 * o - 1)) == 0 && l + o < 32) lp = op_combine(g, lp, rr, err, p0);
+            const int64_t rr = __shfl_down_sync(0xffffffffu, lv, o);
+            if ((l & (2 * o - 1)) == 0) lv = op_apply(g, lv, rr, err, p0);
         }
-        if (l == 0) s_w[w] = lp;
-        __syncthreads();
-        if (threadIdx.x == 0)
-            for (int q = 0; q < nw; ++q) acc = op_combine(g, acc, s_w[q], err, r0);
-        __syncthreads();
+        if (l == 0) {
+            OPart bp;
+            bp.v = lv;
+            bp.has = 1;
+            acc = op_combine(g, acc, bp, err, r0);
+        }
+    }
+    if (wfull < whi) {                            // ragged / unaligned rest, element by element
+        for (int64_t r0 = wfull; r0 < whi; r0 += RW) {
+            const int64_t p0 = r0 + (int64_t)l * (4 * UP);
+            OPart lp;
+            lp.v = 0;
+            lp.has = 0;
+#pragma unroll
+            for (int u = 0; u < UP; ++u) {
+                TX xe4[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int64_t q = p0 + 4 * u + e;
+                    xe4[e] = q < whi ? x[q] : x[wlo];
+                }
+                typename F::Res r[4];
+                int code[4] = {0, 0, 0, 0};
+                f(xe4, p0 + 4 * u, r, code);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int64_t q = p0 + 4 * u + e;
+                    if (q >= whi) break;
+                    if (code[e]) { raise_err(err, q, code[e]); continue; }
+                    OPart v;
+                    v.v = to_reg(r[e]);
+                    v.has = 1;
+                    lp = op_combine(g, lp, v, err, q);
+                }
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                OPart rr;
+                rr.v = __shfl_down_sync(0xffffffffu, lp.v, o);
+                rr.has = __shfl_down_sync(0xffffffffu, lp.has, o);
+                if ((l & (2 * o - 1)) == 0 && l + o < 32) lp = op_combine(g, lp, rr, err, p0);
+            }
+            if (l == 0) acc = op_combine(g, acc, lp, err, r0);
+        }
+    }
+    if (l == 0) s_w[w] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        OPart c = s_w[0];
+        for (int q = 1; q < nw; ++q) c = op_combine(g, c, s_w[q], err, lo);
+        acc = c;
     }
     __shared__ bool s_last;
     if (threadIdx.x == 0) {

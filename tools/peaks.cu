@@ -66,6 +66,20 @@ __global__ void k_lds(double* out, int s) {
     if (acc.x + acc.y + acc.z + acc.w == 1.2345f) out[0] = acc.x;
 }
 
+// L2 read bandwidth: the grid streams an L2-resident buffer (ld.global.cg,
+// 16-B vectors, 4 independent loads per thread per iteration), `passes` times.
+__global__ void k_l2(const float4* __restrict__ buf, size_t n4, int passes, double* out) {
+    float4 acc = make_float4(0, 0, 0, 0);
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (int p = 0; p < passes; ++p)
+        for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i + 3 * stride < n4; i += 4 * stride) {
+            const float4 v0 = __ldcg(buf + i), v1 = __ldcg(buf + i + stride);
+            const float4 v2 = __ldcg(buf + i + 2 * stride), v3 = __ldcg(buf + i + 3 * stride);
+            acc.x += v0.x + v1.x; acc.y += v0.y + v2.y; acc.z += v1.z + v3.z; acc.w += v2.w + v3.w;
+        }
+    if (acc.x + acc.y + acc.z + acc.w == 1.2345f) out[0] = acc.x;
+}
+
 template <class F>
 static double best_ms(F launch) {
     cudaEvent_t a, b;
@@ -100,13 +114,20 @@ int main() {
     const double ex2 = lanes_ops / (best_ms([&] { k_ex2<<<grid, thr>>>(out, 0.f); }) * 1e-3);
     const double lds = (double)grid * thr * (ITERS / 4) * CH * 16 /
                        (best_ms([&] { k_lds<<<grid, thr>>>(out, 1); }) * 1e-3);
+    const size_t l2n4 = (size_t)4 * sms * 512 * 4 * 24;   // 24 iterations per thread: ~58 MiB
+    float4* l2buf;
+    cudaMalloc(&l2buf, l2n4 * 16);
+    cudaMemset(l2buf, 0, l2n4 * 16);
+    const double l2 = 8.0 * l2n4 * 16 / (best_ms([&] { k_l2<<<4 * sms, 512>>>(l2buf, l2n4, 8, out); }) * 1e-3);
+    const size_t l2s = l2n4 / 4;                           // ~14.5 MiB: inside one die's L2 half
+    const double l2small = 32.0 * l2s * 16 / (best_ms([&] { k_l2<<<4 * sms, 512>>>(l2buf, l2s, 32, out); }) * 1e-3);
     const double hz = clk * 1e3;
     printf("{\"sms\": %d, \"clock_mhz_attr\": %.0f, "
            "\"fp64_add_ops_per_s\": %.4e, \"fp64_fma_flops_per_s\": %.4e, \"fp32_fma_flops_per_s\": %.4e, "
-           "\"mufu_ex2_per_s\": %.4e, \"smem_load_bytes_per_s\": %.4e, "
+           "\"mufu_ex2_per_s\": %.4e, \"smem_load_bytes_per_s\": %.4e, \"l2_read_bytes_per_s\": %.4e, \"l2_read_bytes_per_s_14MiB\": %.4e, "
            "\"per_sm_per_clk_at_attr_clock\": {\"fp64_add\": %.1f, \"fp64_fma\": %.1f, \"fp32_fma\": %.1f, "
            "\"mufu_ex2\": %.1f, \"smem_load_B\": %.1f}}\n",
-           sms, hz / 1e6, dadd, 2 * dfma, 2 * ffma, ex2, lds, dadd / sms / hz, dfma / sms / hz, ffma / sms / hz,
+           sms, hz / 1e6, dadd, 2 * dfma, 2 * ffma, ex2, lds, l2, l2small, dadd / sms / hz, dfma / sms / hz, ffma / sms / hz,
            ex2 / sms / hz, lds / sms / hz);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { fprintf(stderr, "%s\n", cudaGetErrorString(e)); return 1; }

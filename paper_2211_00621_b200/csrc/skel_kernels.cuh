@@ -642,10 +642,14 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
     if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(bar, 1u);
+        // spin with relaxed loads (an acquire load per iteration would invalidate
+        // this SM's L1 each time, under the CTAs still working on it), then one
+        // acquire fence
         unsigned v;
         do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
         } while (v < target);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
 }

@@ -189,23 +189,29 @@ k_nn_grad(const double* __restrict__ x, const int* __restrict__ y, const double*
             const double* xc = xs + 4 * tbi + g * nin;
             const double* dc = dzs + 4 * tbj + g * NN_MAXOUT;
             const int xstep = G * nin, dstep = G * NN_MAXOUT;
-            for (int pl = g; pl < npt; pl += G, xc += xstep, dc += dstep) {
-                double xv[4];
-                if ((nin & 1) == 0) {
-                    const double2 a = *reinterpret_cast<const double2*>(xc);
-                    const double2 c = *reinterpret_cast<const double2*>(xc + 2);
-                    xv[0] = a.x; xv[1] = a.y; xv[2] = c.x; xv[3] = c.y;
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) xv[u] = xc[u];
-                }
-                const double2 d01 = *reinterpret_cast<const double2*>(dc);
-                const double2 d23 = *reinterpret_cast<const double2*>(dc + 2);
+            auto mac = [&](const double (&xv)[4], const double* d) {
+                const double2 d01 = *reinterpret_cast<const double2*>(d);
+                const double2 d23 = *reinterpret_cast<const double2*>(d + 2);
                 const double dv[4] = {d01.x, d01.y, d23.x, d23.y};
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
 #pragma unroll
                     for (int v = 0; v < 4; ++v) dwacc[u * 4 + v] = __fma_rn(xv[u], dv[v], dwacc[u * 4 + v]);
+            };
+            if ((nin & 1) == 0) {                          // x rows 16-byte aligned
+#pragma unroll 4
+                for (int pl = g; pl < npt; pl += G, xc += xstep, dc += dstep) {
+                    const double2 a = *reinterpret_cast<const double2*>(xc);
+                    const double2 c = *reinterpret_cast<const double2*>(xc + 2);
+                    const double xv[4] = {a.x, a.y, c.x, c.y};
+                    mac(xv, dc);
+                }
+            } else {
+#pragma unroll 4
+                for (int pl = g; pl < npt; pl += G, xc += xstep, dc += dstep) {
+                    const double xv[4] = {xc[0], xc[1], xc[2], xc[3]};
+                    mac(xv, dc);
+                }
             }
         }
         __syncthreads();                                   // xs[it & 1] and dzs free

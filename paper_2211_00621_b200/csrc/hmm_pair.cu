@@ -104,8 +104,12 @@ __device__ __forceinline__ uint32_t hp_u_offset(int s, int i) {
 // epilogue finishes M block mb it releases those rows of u_t to its own UMMAs
 // (ublk[mb]) and bulk-copies them (16 KiB) to the peer (upeer[mb] there); the
 // K blocks of a step run per M block: mine, then the peer's.
-template <bool OVL>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HP_THREADS, 1)
+// CL = 4: two pairs per cluster (different signals); the CTAs holding the same
+// half of the states in both pairs need the same A^T tiles, so each loads half
+// of every tile (64 rows) and multicasts it to both: A^T is read from L2 once
+// per two pairs (the pair kernel is L2 -> SM bound: ncu xbar2l1 ~10.5 TB/s).
+template <bool OVL, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(HP_THREADS, 1)
 k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ E_lin,
                const float* __restrict__ pi_lin, int K, const int* __restrict__ obs, int64_t nsig, int T,
                double* __restrict__ out_ll) {
@@ -113,14 +117,18 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
     extern __shared__ uint8_t smem_raw[];
     HpSmem& Sm = *reinterpret_cast<HpSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = tc::cluster_ctarank();
-    const uint32_t peer = rank ^ 1u;
+    const uint32_t crank = tc::cluster_ctarank();
+    const uint32_t peer = crank ^ 1u;                // the other half of my pair
+    const uint32_t rank = crank & 1u;                // my half of the states
+    const uint32_t pidx = crank >> 1;                // my pair within the cluster (CL = 4)
+    const uint16_t mc_mask = (uint16_t)((1u << rank) | (1u << (rank + 2)));   // same half, both pairs
     const int64_t s0 = (int64_t)(blockIdx.x >> 1) * HP_N;
     const int j0 = (int)rank * HP_HALF;              // first output state of this CTA
 
     if (threadIdx.x < HP_N) Sm.inv_c[threadIdx.x] = 1.f;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < HP_ST; ++s) { tc::mbar_init(&Sm.full[s], 1); tc::mbar_init(&Sm.empty[s], 1); }
+        // CL = 4: a stage is free when the MMAs of both CTAs sharing its tiles consumed it
+        for (int s = 0; s < HP_ST; ++s) { tc::mbar_init(&Sm.full[s], 1); tc::mbar_init(&Sm.empty[s], CL == 4 ? 2 : 1); }
         tc::mbar_init(&Sm.dfull, 1);
         // uready: two arrivals (armed with the peer copy's bytes; own u written) + the copy's tx
         tc::mbar_init(&Sm.uready, OVL ? 1 : 2);
@@ -150,10 +158,14 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                         // K block order: mine first (OVL), then the peer's
                         // OVL K block order: per M block g of the producing epilogue, my
                         // two K blocks then the peer's two
-                        const int kb = OVL ? (int)((ki & 3) < 2 ? rank : peer) * 8 + 2 * (ki >> 2) + (ki & 1) : ki;
+                        const int kb = OVL ? (int)((ki & 3) < 2 ? rank : (rank ^ 1u)) * 8 + 2 * (ki >> 2) + (ki & 1) : ki;
                         tc::mbar_wait(&Sm.empty[stage], phase ^ 1);
                         tc::mbar_arrive_expect_tx(&Sm.full[stage], HP_TILE);
-                        tc::tma_load_2d(Sm.At[stage], &tmA, &Sm.full[stage], kb * HP_KB, j0 + mb * HP_M);
+                        if (CL == 4)                 // my 64 rows of the tile, to both CTAs of my half
+                            tc::tma_load_2d_mc(Sm.At[stage] + pidx * (HP_M / 2) * HP_KB, &tmA, &Sm.full[stage],
+                                               kb * HP_KB, j0 + mb * HP_M + (int)pidx * (HP_M / 2), mc_mask);
+                        else
+                            tc::tma_load_2d(Sm.At[stage], &tmA, &Sm.full[stage], kb * HP_KB, j0 + mb * HP_M);
                         if (++stage == HP_ST) { stage = 0; phase ^= 1; }
                     }
         }
@@ -172,7 +184,7 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 int kb = ki;
                 if (OVL) {
                     const int g = ki >> 2, w = ki & 3;
-                    kb = (int)(w < 2 ? rank : peer) * 8 + 2 * g + (w & 1);
+                    kb = (int)(w < 2 ? rank : (rank ^ 1u)) * 8 + 2 * g + (w & 1);
                     if (w == 0) {                                 // my M block g of u_{t-1} written
                         tc::mbar_wait(&Sm.ublk[g], (uint32_t)((t - 1) & 1));
                         tc::tc_fence_after();
@@ -198,7 +210,8 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                             for (int kk = 0; kk < HP_KB / 16; ++kk)
                                 tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb >= 2) || (kk != 0));
                         }
-                        tc::umma_commit(&Sm.empty[stage]);
+                        if (CL == 4) tc::umma_commit_mc(&Sm.empty[stage], mc_mask);
+                        else tc::umma_commit(&Sm.empty[stage]);
                     }
                     __syncwarp();
                     if (++stage == HP_ST) { stage = 0; phase ^= 1; }
@@ -351,7 +364,7 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         if (rank == 0 && ew < 2 && s0 + ew * 32 + lane < nsig) out_ll[s0 + ew * 32 + lane] = ll;
     }
     tc::tc_fence_before();
-    tc::cluster_sync();                      // no CTA leaves while the peer may still write into it
+    tc::cluster_sync();                      // no CTA leaves while a peer may still write into it
     if (warp == 2) tc::tmem_dealloc(tmem, 512);
 }
 
@@ -370,20 +383,30 @@ int hmm_pair_launch(const float* log_pi, const float* A, const float* log_E, int
     k_hmm_tc_prep<__half><<<dim3(S / 32, S / 32), dim3(32, 8), 0, st>>>(A, log_E, log_pi, S, K, At, E_lin, pi_lin);
     PMX_CHECK_LAUNCH("hmm_pair_prep");
     CUtensorMap tmA;
-    if (!make_tmap_2d(&tmA, At, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (uint64_t)S, (uint64_t)S, HP_M, HP_KB,
-                      CU_TENSOR_MAP_SWIZZLE_128B)) {
+    static const bool mc_map = !(getenv("PMX_HMM_PAIR_MC") && getenv("PMX_HMM_PAIR_MC")[0] == '0') &&
+                               !(getenv("PMX_HMM_PAIR_SERIAL") && getenv("PMX_HMM_PAIR_SERIAL")[0] == '1');
+    if (!make_tmap_2d(&tmA, At, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (uint64_t)S, (uint64_t)S,
+                      mc_map ? HP_M / 2 : HP_M, HP_KB, CU_TENSOR_MAP_SWIZZLE_128B)) {
         set_last_error("hmm_pair: cuTensorMapEncodeTiled failed");
         return -2;
     }
-    const unsigned grid = (unsigned)(2 * ((nsig + HP_N - 1) / HP_N));
     const size_t smem = sizeof(HpSmem) + 1024;
     static const bool serial = getenv("PMX_HMM_PAIR_SERIAL") && getenv("PMX_HMM_PAIR_SERIAL")[0] == '1';
+    static const bool mc = !(getenv("PMX_HMM_PAIR_MC") && getenv("PMX_HMM_PAIR_MC")[0] == '0');
+    const int64_t pairs = (nsig + HP_N - 1) / HP_N;
     if (serial) {
-        cudaFuncSetAttribute(k_hmm_fwd_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_hmm_fwd_pair<false><<<grid, HP_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
+        const unsigned grid = (unsigned)(2 * pairs);
+        cudaFuncSetAttribute(k_hmm_fwd_pair<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_hmm_fwd_pair<false, 2><<<grid, HP_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
+    } else if (!mc) {
+        const unsigned grid = (unsigned)(2 * pairs);
+        cudaFuncSetAttribute(k_hmm_fwd_pair<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_hmm_fwd_pair<true, 2><<<grid, HP_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
     } else {
-        cudaFuncSetAttribute(k_hmm_fwd_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_hmm_fwd_pair<true><<<grid, HP_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
+        // whole clusters of two pairs (a padding pair runs on masked signals)
+        const unsigned grid = (unsigned)(4 * ((pairs + 1) / 2));
+        cudaFuncSetAttribute(k_hmm_fwd_pair<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_hmm_fwd_pair<true, 4><<<grid, HP_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
     }
     PMX_CHECK_LAUNCH("hmm_fwd_pair");
     return 0;

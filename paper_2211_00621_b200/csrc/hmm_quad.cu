@@ -1,0 +1,370 @@
+// HMM forward on the tensor cores, 4-CTA variant with CTA-pair UMMA
+// (tcgen05 cta_group::2).  Same recursion, scaling and fp16 operands as
+// hmm_tc.cu / hmm_pair.cu (see hmm_tc.cu for the reference anchor and the
+// precision argument).
+//
+// Why: at M = 128, N = 64 (hmm_pair.cu) a UMMA needs 6 KiB of shared-memory
+// operands per 32 clocks — more than the 128 B/clk an SM's shared memory
+// delivers (tools/umma_rate.cu: N = 64 issues at 1.46 PFLOP/s, N = 128 at
+// 2.2) — and every SM also streams 1 MiB of A^T per step.  A pair UMMA
+// (M = 256, N = 128) takes its A rows from both SMs of a pair and splits the
+// N = 128 signal columns of u between them (64 each: the 128 KiB B buffer of
+// hmm_pair.cu), so each SM reads 6 KiB per 64 clocks; two pairs in a cluster
+// split the states, so each SM streams 256 rows (512 KiB) of A^T per step.
+//
+// Layout (cluster of 4, 128 signals): CTA c = 2p + h.  Pair p owns output
+// states [512p, 512p + 512) as two M blocks of 256 rows; in M block mb, CTA h
+// holds rows 512p + 256mb + 128h + [0, 128) of A^T (its TMEM lanes) and B
+// columns (signals) 64h + [0, 64) for all 1024 states (K).  D (fp32, TMEM):
+// lanes = this CTA's 128 states of the M block, columns = the 128 signals.
+//
+// Per step t (u_{t-1} complete in all four B buffers):
+//   producers (both CTAs of a pair): A^T tiles by TMA (cta_group::2: the
+//                bytes complete on the pair leader's `full`)
+//   MMA (leader): 2 M blocks x 16 K blocks x 4 UMMA (K = 16), commit to both
+//                CTAs' `empty`, finally to both CTAs' `dfull`
+//   epilogue (8 warps per CTA: TMEM lane quadrant x signal half):
+//     a. wait dfull(t); arrive on `mdone` of all four CTAs; wait mine (every
+//        pair's MMAs of t are done: nobody reads u_{t-1} any more)
+//     b. per M block: u_t = D * E(o_t) * 1/c_{t-1} -> fp16; my signal half
+//        into my own B, the other half into a staging buffer; bulk copies:
+//        my B rows -> the other pair's CTA of my half, the staging rows ->
+//        both CTAs of the other half (complete_tx on their `uready`)
+//     c. per-signal partial sums -> all four CTAs (st.async, `psum`); c_t =
+//        the four partials added in CTA order (identical everywhere)
+//   the leader's MMAs of t+1 wait its `uready` and the partner's (`pready`).
+#include <cuda_fp16.h>
+#include <stdlib.h>
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace pmx {
+
+constexpr int HQ_N = 128;            // signals per cluster (UMMA N)
+constexpr int HQ_NH = 64;            // signals in one CTA's B buffer
+constexpr int HQ_M = 128;            // A^T rows per CTA per UMMA (M = 256 per pair)
+constexpr int HQ_KB = 64;            // fp16 per 128-byte swizzle row
+constexpr int HQ_S = 1024;
+constexpr int HQ_NKB = HQ_S / HQ_KB;   // 16 K blocks
+constexpr int HQ_MB = 2;             // M blocks (256 states) per pair
+constexpr int HQ_ST = 4;             // TMA ring stages
+constexpr int HQ_KMAX = 8;
+constexpr int HQ_EW = 8;             // epilogue warps (4 TMEM lane quadrants x 2 signal halves)
+constexpr int HQ_THREADS = 128 + 32 * HQ_EW;
+constexpr uint32_t HQ_TILE = HQ_M * 128;                 // 16 KiB of A^T per CTA per stage
+constexpr uint32_t HQ_ROWS = 2 * HQ_NH * 128;            // 16 KiB: 2 K blocks x 64 signals (128 states)
+
+struct __align__(1024) HqSmem {
+    __half U[HQ_NKB][HQ_NH * HQ_KB];     // B operand: K-major SW128 [kblock][signal][64]
+    __half At[HQ_ST][HQ_M * HQ_KB];      // A operand tiles
+    __half X[2][HQ_NH * HQ_KB];          // staging: the other signal half of one M block
+    float wsum[4][HQ_N];                 // per TMEM lane quadrant partial sums
+    float psum_in[2][4][HQ_N];           // [step parity][source CTA][signal]
+    float inv_c[HQ_N];
+    int sym[HQ_N];
+    uint64_t full[HQ_ST], empty[HQ_ST];
+    uint64_t dfull, uready, pready, mdone, psum;
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t hq_mapa(uint32_t smem_addr, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void hq_arrive_remote(uint32_t remote_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void hq_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}"
+        :: "r"(tc::smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void hq_st_async(uint32_t remote_addr, float v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+                 :: "r"(remote_addr), "r"(__float_as_uint(v)), "r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void hq_bulk_to(uint32_t remote_dst, const void* src, uint32_t bytes, uint32_t remote_bar) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(remote_dst), "r"(tc::smem_u32(src)), "r"(bytes), "r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void hq_bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void hq_bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+// pair (cta_group::2) forms of the tcgen05 / TMA operations
+__device__ __forceinline__ void hq_tmem_alloc2(uint32_t* holder, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(tc::smem_u32(holder)), "r"(ncols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void hq_tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void hq_umma2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void hq_commit2(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 :: "r"(tc::smem_u32(bar)), "h"(mask) : "memory");
+}
+// TMA tile into this CTA's shared memory; the bytes complete on `bar_cluster`
+// (the pair leader's barrier, a shared::cluster address)
+__device__ __forceinline__ void hq_tma_load2(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];"
+        :: "r"(tc::smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(HQ_THREADS, 1)
+k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ E_lin,
+               const float* __restrict__ pi_lin, int K, const int* __restrict__ obs, int64_t nsig, int T,
+               double* __restrict__ out_ll) {
+    constexpr float kOut = 1.f / 1024.f, kSum = 1.f / 1024.f, kInit = 1048576.f;
+    extern __shared__ uint8_t smem_raw[];
+    HqSmem& Sm = *reinterpret_cast<HqSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = tc::cluster_ctarank();
+    const uint32_t p = crank >> 1, h = crank & 1u;
+    const uint32_t leader = crank & ~1u;                       // this pair's MMA issuer
+    const uint16_t pair_mask = (uint16_t)(3u << (2 * p));
+    const int64_t s0 = (int64_t)(blockIdx.x >> 2) * HQ_N;
+    auto jbase = [&](int mb) { return (int)(512 * p + 256 * mb + 128 * h); };   // my first state of M block mb
+
+    if (threadIdx.x < HQ_N) Sm.inv_c[threadIdx.x] = 1.f;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < HQ_ST; ++s) { tc::mbar_init(&Sm.full[s], 1); tc::mbar_init(&Sm.empty[s], 1); }
+        tc::mbar_init(&Sm.dfull, 1);
+        tc::mbar_init(&Sm.uready, 1);
+        tc::mbar_init(&Sm.pready, 1);
+        tc::mbar_init(&Sm.mdone, 4);
+        tc::mbar_init(&Sm.psum, 1);
+        tc::fence_mbar_init();
+        tc::tma_prefetch(&tmA);
+    }
+    if (warp == 2) hq_tmem_alloc2(&Sm.tmem_base, 256);
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    tc::tc_fence_after();
+    const uint32_t tmem = Sm.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {                                     // ---- TMA producer (both CTAs of a pair)
+            const uint32_t lead_full0 = hq_mapa(tc::smem_u32(&Sm.full[0]), leader);
+            int stage = 0; uint32_t phase = 0;
+            for (int t = 1; t < T; ++t)
+                for (int mb = 0; mb < HQ_MB; ++mb)
+                    for (int kb = 0; kb < HQ_NKB; ++kb) {
+                        tc::mbar_wait(&Sm.empty[stage], phase ^ 1);
+                        if (h == 0) tc::mbar_arrive_expect_tx(&Sm.full[stage], 2 * HQ_TILE);
+                        hq_tma_load2(Sm.At[stage], &tmA, lead_full0 + (uint32_t)(stage * sizeof(uint64_t)),
+                                     kb * HQ_KB, jbase(mb));
+                        if (++stage == HQ_ST) { stage = 0; phase ^= 1; }
+                    }
+        }
+    } else if (warp == 1) {
+        if (h == 0) {                                        // ---- MMA issuer (pair leader)
+            constexpr uint32_t idesc = tc::instr_desc(2 * HQ_M, HQ_N, 0);
+            int stage = 0; uint32_t phase = 0;
+            const uint64_t u_desc = tc::sw128_kmajor_desc(tc::smem_u32(&Sm.U[0][0]));
+            const uint64_t at_desc = tc::sw128_kmajor_desc(tc::smem_u32(Sm.At[0]));
+            for (int t = 1; t < T; ++t) {
+                tc::mbar_wait(&Sm.uready, (uint32_t)((t - 1) & 1));   // my B holds u_{t-1}
+                hq_wait_cluster(&Sm.pready, (uint32_t)((t - 1) & 1)); // and the partner's
+                tc::tc_fence_after();
+                for (int mb = 0; mb < HQ_MB; ++mb) {
+                    const uint32_t d = tmem + (uint32_t)(mb * HQ_N);
+                    for (int kb = 0; kb < HQ_NKB; ++kb) {
+                        tc::mbar_wait(&Sm.full[stage], phase);
+                        tc::tc_fence_after();
+                        if (tc::elect_one()) {
+                            const uint64_t ad = at_desc + (uint64_t)(stage * (HQ_TILE >> 4));
+                            const uint64_t bd = u_desc + (uint64_t)(kb * ((HQ_NH * 128) >> 4));
+#pragma unroll
+                            for (int kk = 0; kk < HQ_KB / 16; ++kk)
+                                hq_umma2(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb > 0) || (kk != 0));
+                            hq_commit2(&Sm.empty[stage], pair_mask);
+                        }
+                        __syncwarp();
+                        if (++stage == HQ_ST) { stage = 0; phase ^= 1; }
+                    }
+                }
+                if (tc::elect_one()) hq_commit2(&Sm.dfull, pair_mask);
+                __syncwarp();
+            }
+        } else if (lane == 0) {                              // partner: forward "my B is ready"
+            const uint32_t lead_pready = hq_mapa(tc::smem_u32(&Sm.pready), leader);
+            for (int t = 1; t < T; ++t) {
+                tc::mbar_wait(&Sm.uready, (uint32_t)((t - 1) & 1));
+                hq_arrive_remote(lead_pready);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---- epilogue: warp w reads TMEM lane quadrant q (states jbase(mb) + 32q + lane)
+        // and the signal half hh (signals 64 hh .. 64 hh + 63, in two chunks of 32)
+        const int q = warp & 3;
+        const int ew = warp - 4;
+        const int hh = ew >> 2;
+        const bool lead = threadIdx.x == 128;
+        double ll = 0.0;
+        uint32_t dpar = 0;
+        const float* __restrict__ Ef = E_lin;
+        uint32_t mdone_bar[4], psum_bar[4], uready_bar[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            mdone_bar[c] = hq_mapa(tc::smem_u32(&Sm.mdone), (uint32_t)c);
+            psum_bar[c] = hq_mapa(tc::smem_u32(&Sm.psum), (uint32_t)c);
+            uready_bar[c] = hq_mapa(tc::smem_u32(&Sm.uready), (uint32_t)c);
+        }
+        const uint32_t same_half_other_pair = crank ^ 2u, other_half_same_pair = crank ^ 1u,
+                       other_half_other_pair = crank ^ 3u;
+        for (int t = 0; t < T; ++t) {
+            if (ew < 4) {
+                const int m = ew * 32 + lane;
+                const int64_t sg = s0 + m;
+                Sm.sym[m] = (sg < nsig) ? obs[sg * T + t] : 0;
+            }
+            if (lead) tc::mbar_arrive_expect_tx(&Sm.psum, 3 * HQ_N * 4);   // this step's partials from 3 CTAs
+            for (int v = ew * 32 + lane; v < 4 * HQ_N; v += 32 * HQ_EW) (&Sm.wsum[0][0])[v] = 0.f;
+            if (t > 0) {
+                tc::mbar_wait(&Sm.dfull, dpar); dpar ^= 1;
+                tc::tc_fence_after();
+                if (lead)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) hq_arrive_remote(mdone_bar[c]);
+                hq_wait_cluster(&Sm.mdone, (uint32_t)((t - 1) & 1));
+            }
+            asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+#pragma unroll 1
+            for (int mb = 0; mb < HQ_MB; ++mb) {
+                const int j = jbase(mb) + q * 32 + lane;
+                const int kb0 = jbase(mb) / HQ_KB;           // first of my two K blocks
+                const uint32_t byte = (uint32_t)(j % HQ_KB) * 2u;
+                const uint32_t chunkj = byte >> 4;
+                uint8_t* dst = hh == (int)h
+                    ? reinterpret_cast<uint8_t*>(&Sm.U[0][0]) + (j / HQ_KB) * (HQ_NH * 128) + (byte & 15)
+                    : reinterpret_cast<uint8_t*>(&Sm.X[0][0]) + (j / HQ_KB - kb0) * (HQ_NH * 128) + (byte & 15);
+#pragma unroll 1
+                for (int ch = 0; ch < 2; ++ch) {             // 32 signals at a time
+                    const int sb = hh * HQ_NH + ch * 32;     // first signal (of the cluster's 128)
+                    float d[32];
+                    if (t > 0) {
+                        uint32_t r[32];
+                        tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mb * HQ_N + sb), r);
+                        tc::tmem_ld_wait();
+#pragma unroll
+                        for (int s = 0; s < 32; ++s) d[s] = __uint_as_float(r[s]);
+                    } else {
+                        const float pv = pi_lin[j] * kInit;
+#pragma unroll
+                        for (int s = 0; s < 32; ++s) d[s] = pv;
+                    }
+                    float csum[32];
+#pragma unroll
+                    for (int s = 0; s < 32; ++s) {
+                        const int sg = sb + s;
+                        const int sl = ch * 32 + s;          // signal within the half (B column)
+                        const __half ur = __float2half_rn(d[s] * __ldg(Ef + Sm.sym[sg] * HQ_S + j) *
+                                                          (Sm.inv_c[sg] * kOut));
+                        csum[s] = __half2float(ur);
+                        *reinterpret_cast<__half*>(dst + sl * 128 + ((chunkj ^ (uint32_t)(sl & 7)) << 4)) = ur;
+                    }
+                    // sums over the warp's 32 states: transpose-reduce, lane l ends with signal sb + l
+#pragma unroll
+                    for (int w = 16; w > 0; w >>= 1) {
+                        const bool upper = (lane & w) != 0;
+#pragma unroll
+                        for (int s = 0; s < w; ++s) {
+                            const float send = upper ? csum[s] : csum[s + w];
+                            const float keep = upper ? csum[s + w] : csum[s];
+                            csum[s] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+                        }
+                    }
+                    Sm.wsum[q][sb + lane] += csum[0];        // M block 0, then 1 (same warp)
+                }
+                tc::tc_fence_before();
+                tc::fence_proxy_async();                     // u_t rows visible to the async proxy
+                asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+                if (lead && t + 1 < T) {
+                    const uint32_t off = (uint32_t)kb0 * (HQ_NH * 128);
+                    const uint8_t* mine = reinterpret_cast<const uint8_t*>(&Sm.U[0][0]) + off;
+                    const uint32_t u0 = tc::smem_u32(&Sm.U[0][0]) + off;
+                    hq_bulk_to(hq_mapa(u0, same_half_other_pair), mine, HQ_ROWS, uready_bar[same_half_other_pair]);
+                    hq_bulk_to(hq_mapa(u0, other_half_same_pair), &Sm.X[0][0], HQ_ROWS,
+                               uready_bar[other_half_same_pair]);
+                    hq_bulk_to(hq_mapa(u0, other_half_other_pair), &Sm.X[0][0], HQ_ROWS,
+                               uready_bar[other_half_other_pair]);
+                    hq_bulk_commit();
+                    hq_bulk_wait_read();                     // staging (and my rows) free again
+                }
+                asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+            }
+            // my partial of every signal -> all four CTAs (own slot written locally)
+            float part = 0.f;
+            if (ew < 4) {
+                const int m = ew * 32 + lane;
+                part = (Sm.wsum[0][m] + Sm.wsum[1][m]) + (Sm.wsum[2][m] + Sm.wsum[3][m]);
+                Sm.psum_in[t & 1][crank][m] = part;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c != (int)crank)
+                        hq_st_async(hq_mapa(tc::smem_u32(&Sm.psum_in[t & 1][crank][m]), (uint32_t)c), part,
+                                    psum_bar[c]);
+            }
+            if (lead && t + 1 < T)                            // my own rows of u_t are written
+                tc::mbar_arrive_expect_tx(&Sm.uready, 3 * HQ_MB * HQ_ROWS);
+            asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+            if (ew < 4) {
+                hq_wait_cluster(&Sm.psum, (uint32_t)(t & 1));
+                const int m = ew * 32 + lane;
+                const float c = ((Sm.psum_in[t & 1][0][m] + Sm.psum_in[t & 1][1][m]) +
+                                 (Sm.psum_in[t & 1][2][m] + Sm.psum_in[t & 1][3][m])) * kSum;
+                Sm.inv_c[m] = 1.f / c;
+                ll += log((double)c);
+            }
+            asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+        }
+        if (crank == 0 && ew < 4 && s0 + ew * 32 + lane < nsig) out_ll[s0 + ew * 32 + lane] = ll;
+    }
+    tc::tc_fence_before();
+    tc::cluster_sync();                      // no CTA leaves while a peer may still write into it
+    if (warp == 2) hq_tmem_dealloc2(tmem, 256);
+}
+
+bool make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t rows,
+                  uint64_t cols, uint32_t box_rows, uint32_t box_cols, CUtensorMapSwizzle swz);
+template <class ET>
+__global__ void k_hmm_tc_prep(const float* __restrict__ A, const float* __restrict__ log_E,
+                              const float* __restrict__ log_pi, int S, int K, ET* __restrict__ At,
+                              float* __restrict__ E_lin, float* __restrict__ pi_lin);
+
+int hmm_quad_launch(const float* log_pi, const float* A, const float* log_E, int S, int K, const int* obs,
+                    int64_t nsig, int T, double* out_ll, void* ws, cudaStream_t st) {
+    __half* At = (__half*)ws;
+    float* E_lin = (float*)((char*)ws + (size_t)S * S * 4);
+    float* pi_lin = E_lin + (size_t)HQ_KMAX * S;
+    k_hmm_tc_prep<__half><<<dim3(S / 32, S / 32), dim3(32, 8), 0, st>>>(A, log_E, log_pi, S, K, At, E_lin, pi_lin);
+    PMX_CHECK_LAUNCH("hmm_quad_prep");
+    CUtensorMap tmA;
+    if (!make_tmap_2d(&tmA, At, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (uint64_t)S, (uint64_t)S, HQ_M, HQ_KB,
+                      CU_TENSOR_MAP_SWIZZLE_128B)) {
+        set_last_error("hmm_quad: cuTensorMapEncodeTiled failed");
+        return -2;
+    }
+    const unsigned grid = (unsigned)(4 * ((nsig + HQ_N - 1) / HQ_N));
+    const size_t smem = sizeof(HqSmem) + 1024;
+    cudaFuncSetAttribute(k_hmm_fwd_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_hmm_fwd_quad<<<grid, HQ_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
+    PMX_CHECK_LAUNCH("hmm_fwd_quad");
+    return 0;
+}
+
+}  // namespace pmx

@@ -324,6 +324,8 @@ static int dbg_flags() {
     return v;
 }
 
+int hmm_quad_launch(const float* log_pi, const float* A, const float* log_E, int S, int K, const int* obs,
+                    int64_t nsig, int T, double* out_ll, void* ws, cudaStream_t st);
 int hmm_pair_launch(const float* log_pi, const float* A, const float* log_E, int S, int K, const int* obs,
                     int64_t nsig, int T, double* out_ll, void* ws, cudaStream_t st);
 
@@ -364,6 +366,8 @@ int hmm_tc_launch(const float* log_pi, const float* A, const float* log_E, int S
     // A^T through smem once per step (TMA write + UMMA read) for only 32
     // signals — fp16 operands halve those bytes.
     static const char* mode = getenv("PMX_HMM_TC");
+    if (mode && !strcmp(mode, "quad"))
+        return hmm_quad_launch(log_pi, A, log_E, S, K, obs, nsig, T, out_ll, ws, st);
     if (!mode || !strcmp(mode, "pair"))
         return hmm_pair_launch(log_pi, A, log_E, S, K, obs, nsig, T, out_ll, ws, st);
     if (mode && !strcmp(mode, "tf32"))

@@ -2,6 +2,7 @@
 CPU oracle.  Tolerances (north_star): integer/index outputs bit-exact, fp64
 rel 1e-9, fp32 rel 1e-5 with log-likelihoods compared in fp64."""
 import math
+import pathlib
 
 import numpy as np
 import pytest
@@ -306,3 +307,30 @@ def test_rk4_trace_into_aliased_tensor_view():
     _, want = O.rk4_trace(ps, synth.RK4_INIT, m, synth.RK4_H, 0)
     assert np.allclose(got[2:n + 2], want, rtol=1e-9, atol=1e-12)
     assert (got[:2] == -7.0).all() and (got[n + 2:] == -7.0).all()
+
+
+@pytest.mark.parametrize("variant", ["quad", "f16", "tf32"])
+def test_hmm_forward_kernel_variants_vs_oracle(variant, tmp_path):
+    """The non-default S = 1024 tensor-core kernels (PMX_HMM_TC, read once per
+    process, so each runs in a subprocess): the 4-CTA pair-UMMA kernel
+    (hmm_quad.cu, cta_group::2), the single-CTA fp16 and TF32 kernels — same
+    signals as the default kernel's precision test, incl. a partial cluster."""
+    import json
+    import os
+    import subprocess
+    import sys
+    A, E, pi = synth.hmm_model(1024, 8)
+    obs = synth.hmm_obs(133, 120, 8)
+    want = O.hmm_forward(A, E, pi, obs)
+    code = ("import json, sys, numpy as np\n"
+            "from paper_2211_00621_b200 import accelerate, hmm_forward, synth\n"
+            "A, E, pi = synth.hmm_model(1024, 8)\n"
+            "obs = synth.hmm_obs(133, 120, 8)\n"
+            "print(json.dumps([float(v) for v in np.asarray(accelerate(hmm_forward, A, E, pi, obs))]))\n")
+    env = dict(os.environ, PMX_HMM_TC=variant)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=str(pathlib.Path(__file__).resolve().parent.parent))
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = np.array(json.loads(r.stdout.strip().splitlines()[-1]))
+    err = np.max(np.abs(got - want) / np.abs(want))
+    assert err < 5e-6, (variant, err)

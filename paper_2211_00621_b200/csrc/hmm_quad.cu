@@ -34,6 +34,7 @@
 //        the four partials added in CTA order (identical everywhere)
 //   the leader's MMAs of t+1 wait its `uready` and the partner's (`pready`).
 #include <cuda_fp16.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include "common.cuh"
 #include "tc.cuh"
@@ -49,7 +50,7 @@ constexpr int HQ_NKB = HQ_S / HQ_KB;   // 16 K blocks
 constexpr int HQ_MB = 2;             // M blocks (256 states) per pair
 constexpr int HQ_ST = 4;             // TMA ring stages
 constexpr int HQ_KMAX = 8;
-constexpr int HQ_EW = 8;             // epilogue warps (4 TMEM lane quadrants x 2 signal halves)
+constexpr int HQ_EW = 16;            // epilogue warps (4 TMEM lane quadrants x 4 signal quarters)
 constexpr int HQ_THREADS = 128 + 32 * HQ_EW;
 constexpr uint32_t HQ_TILE = HQ_M * 128;                 // 16 KiB of A^T per CTA per stage
 constexpr uint32_t HQ_ROWS = 2 * HQ_NH * 128;            // 16 KiB: 2 K blocks x 64 signals (128 states)
@@ -63,7 +64,9 @@ struct __align__(1024) HqSmem {
     float inv_c[HQ_N];
     int sym[HQ_N];
     uint64_t full[HQ_ST], empty[HQ_ST];
-    uint64_t dfull, uready, pready, mdone, psum;
+    uint64_t ur[4][2];                   // rows of u_t from CTA c's M block mb in my B (local or copied)
+    uint64_t pr[4][2];                   // (pair leader) the same group landed in the partner's B
+    uint64_t dfull, mdone, psum;
     uint32_t tmem_base;
 };
 
@@ -127,7 +130,7 @@ __device__ __forceinline__ void hq_tma_load2(void* dst, const CUtensorMap* m, ui
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(HQ_THREADS, 1)
 k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ E_lin,
                const float* __restrict__ pi_lin, int K, const int* __restrict__ obs, int64_t nsig, int T,
-               double* __restrict__ out_ll) {
+               double* __restrict__ out_ll, unsigned long long* __restrict__ trace) {
     constexpr float kOut = 1.f / 1024.f, kSum = 1.f / 1024.f, kInit = 1048576.f;
     extern __shared__ uint8_t smem_raw[];
     HqSmem& Sm = *reinterpret_cast<HqSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -137,20 +140,32 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
     const uint32_t leader = crank & ~1u;                       // this pair's MMA issuer
     const uint16_t pair_mask = (uint16_t)(3u << (2 * p));
     const int64_t s0 = (int64_t)(blockIdx.x >> 2) * HQ_N;
+    // PMX_HMM_QUAD_TRACE: %globaltimer stamps of cluster 0, CTA 0, steps < 64 (timeline debugging)
+    auto stamp = [&](int t, int k) {
+        if (trace && blockIdx.x < 4 && t < 64) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+            trace[blockIdx.x * 1024 + t * 16 + k] = g;
+        }
+    };
     auto jbase = [&](int mb) { return (int)(512 * p + 256 * mb + 128 * h); };   // my first state of M block mb
+    // K blocks of u_t produced by CTA c's M block mb (its 128 states)
+    auto kbgrp = [](uint32_t c, int mb) { return (int)(8 * (c >> 1) + 4 * mb + 2 * (c & 1)); };
+    // The MMAs of a step consume K in the order the rows of u_{t-1} become ready:
+    // source M block 0 of the four CTAs (own pair first), then M block 1.
 
     if (threadIdx.x < HQ_N) Sm.inv_c[threadIdx.x] = 1.f;
     if (threadIdx.x == 0) {
         for (int s = 0; s < HQ_ST; ++s) { tc::mbar_init(&Sm.full[s], 1); tc::mbar_init(&Sm.empty[s], 1); }
         tc::mbar_init(&Sm.dfull, 1);
-        tc::mbar_init(&Sm.uready, 1);
-        tc::mbar_init(&Sm.pready, 1);
+        for (int c = 0; c < 4; ++c)
+            for (int b = 0; b < HQ_MB; ++b) { tc::mbar_init(&Sm.ur[c][b], 1); tc::mbar_init(&Sm.pr[c][b], 1); }
         tc::mbar_init(&Sm.mdone, 4);
         tc::mbar_init(&Sm.psum, 1);
         tc::fence_mbar_init();
         tc::tma_prefetch(&tmA);
     }
-    if (warp == 2) hq_tmem_alloc2(&Sm.tmem_base, 256);
+    if (warp == 2) hq_tmem_alloc2(&Sm.tmem_base, 512);   // D double-buffered by step parity
     tc::tc_fence_before();
     tc::cluster_sync();
     tc::tc_fence_after();
@@ -161,14 +176,17 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
             const uint32_t lead_full0 = hq_mapa(tc::smem_u32(&Sm.full[0]), leader);
             int stage = 0; uint32_t phase = 0;
             for (int t = 1; t < T; ++t)
-                for (int mb = 0; mb < HQ_MB; ++mb)
-                    for (int kb = 0; kb < HQ_NKB; ++kb) {
-                        tc::mbar_wait(&Sm.empty[stage], phase ^ 1);
-                        if (h == 0) tc::mbar_arrive_expect_tx(&Sm.full[stage], 2 * HQ_TILE);
-                        hq_tma_load2(Sm.At[stage], &tmA, lead_full0 + (uint32_t)(stage * sizeof(uint64_t)),
-                                     kb * HQ_KB, jbase(mb));
-                        if (++stage == HQ_ST) { stage = 0; phase ^= 1; }
-                    }
+                for (int mbs = 0; mbs < HQ_MB; ++mbs)
+                    for (int i = 0; i < 4; ++i)
+                        for (int k2 = 0; k2 < 2; ++k2)
+                            for (int mbo = 0; mbo < HQ_MB; ++mbo) {
+                                const int kb = kbgrp(leader ^ (uint32_t)i, mbs) + k2;
+                                tc::mbar_wait(&Sm.empty[stage], phase ^ 1);
+                                if (h == 0) tc::mbar_arrive_expect_tx(&Sm.full[stage], 2 * HQ_TILE);
+                                hq_tma_load2(Sm.At[stage], &tmA, lead_full0 + (uint32_t)(stage * sizeof(uint64_t)),
+                                             kb * HQ_KB, jbase(mbo));
+                                if (++stage == HQ_ST) { stage = 0; phase ^= 1; }
+                            }
         }
     } else if (warp == 1) {
         if (h == 0) {                                        // ---- MMA issuer (pair leader)
@@ -177,52 +195,63 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
             const uint64_t u_desc = tc::sw128_kmajor_desc(tc::smem_u32(&Sm.U[0][0]));
             const uint64_t at_desc = tc::sw128_kmajor_desc(tc::smem_u32(Sm.At[0]));
             for (int t = 1; t < T; ++t) {
-                tc::mbar_wait(&Sm.uready, (uint32_t)((t - 1) & 1));   // my B holds u_{t-1}
-                hq_wait_cluster(&Sm.pready, (uint32_t)((t - 1) & 1)); // and the partner's
-                tc::tc_fence_after();
-                for (int mb = 0; mb < HQ_MB; ++mb) {
-                    const uint32_t d = tmem + (uint32_t)(mb * HQ_N);
-                    for (int kb = 0; kb < HQ_NKB; ++kb) {
-                        tc::mbar_wait(&Sm.full[stage], phase);
+                const uint32_t dstep = tmem + (uint32_t)((t & 1) * (HQ_MB * HQ_N));
+                bool first[HQ_MB] = {true, true};
+                for (int mbs = 0; mbs < HQ_MB; ++mbs)
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t c = leader ^ (uint32_t)i;
+                        tc::mbar_wait(&Sm.ur[c][mbs], (uint32_t)((t - 1) & 1));      // in my B
+                        hq_wait_cluster(&Sm.pr[c][mbs], (uint32_t)((t - 1) & 1));    // and the partner's
                         tc::tc_fence_after();
-                        if (tc::elect_one()) {
-                            const uint64_t ad = at_desc + (uint64_t)(stage * (HQ_TILE >> 4));
-                            const uint64_t bd = u_desc + (uint64_t)(kb * ((HQ_NH * 128) >> 4));
+                        if (t < 64 && mbs == 0 && i == 0 && lane == 0) stamp(t, 8);
+                        for (int k2 = 0; k2 < 2; ++k2)
+                            for (int mbo = 0; mbo < HQ_MB; ++mbo) {
+                                const int kb = kbgrp(c, mbs) + k2;
+                                tc::mbar_wait(&Sm.full[stage], phase);
+                                tc::tc_fence_after();
+                                if (tc::elect_one()) {
+                                    const uint64_t ad = at_desc + (uint64_t)(stage * (HQ_TILE >> 4));
+                                    const uint64_t bd = u_desc + (uint64_t)(kb * ((HQ_NH * 128) >> 4));
+                                    const uint32_t d = dstep + (uint32_t)(mbo * HQ_N);
 #pragma unroll
-                            for (int kk = 0; kk < HQ_KB / 16; ++kk)
-                                hq_umma2(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb > 0) || (kk != 0));
-                            hq_commit2(&Sm.empty[stage], pair_mask);
-                        }
-                        __syncwarp();
-                        if (++stage == HQ_ST) { stage = 0; phase ^= 1; }
+                                    for (int kk = 0; kk < HQ_KB / 16; ++kk)
+                                        hq_umma2(d, ad + 2 * kk, bd + 2 * kk, idesc, (!first[mbo]) || (kk != 0));
+                                    hq_commit2(&Sm.empty[stage], pair_mask);
+                                }
+                                __syncwarp();
+                                first[mbo] = false;
+                                if (++stage == HQ_ST) { stage = 0; phase ^= 1; }
+                            }
                     }
-                }
+                if (lane == 0) stamp(t, 10);
                 if (tc::elect_one()) hq_commit2(&Sm.dfull, pair_mask);
                 __syncwarp();
             }
         } else if (lane == 0) {                              // partner: forward "my B is ready"
-            const uint32_t lead_pready = hq_mapa(tc::smem_u32(&Sm.pready), leader);
-            for (int t = 1; t < T; ++t) {
-                tc::mbar_wait(&Sm.uready, (uint32_t)((t - 1) & 1));
-                hq_arrive_remote(lead_pready);
-            }
+            for (int t = 1; t < T; ++t)
+                for (int mbs = 0; mbs < HQ_MB; ++mbs)
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t c = leader ^ (uint32_t)i;
+                        tc::mbar_wait(&Sm.ur[c][mbs], (uint32_t)((t - 1) & 1));
+                        hq_arrive_remote(hq_mapa(tc::smem_u32(&Sm.pr[c][mbs]), leader));
+                    }
         }
     } else if (warp >= 4) {
         // ---- epilogue: warp w reads TMEM lane quadrant q (states jbase(mb) + 32q + lane)
         // and the signal half hh (signals 64 hh .. 64 hh + 63, in two chunks of 32)
         const int q = warp & 3;
         const int ew = warp - 4;
-        const int hh = ew >> 2;
+        const int hq = ew >> 2;                          // signal quarter: signals 32 hq .. 32 hq + 31
+        const int hh = hq >> 1;                          // ... in signal half hh
         const bool lead = threadIdx.x == 128;
         double ll = 0.0;
         uint32_t dpar = 0;
         const float* __restrict__ Ef = E_lin;
-        uint32_t mdone_bar[4], psum_bar[4], uready_bar[4];
+        uint32_t mdone_bar[4], psum_bar[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             mdone_bar[c] = hq_mapa(tc::smem_u32(&Sm.mdone), (uint32_t)c);
             psum_bar[c] = hq_mapa(tc::smem_u32(&Sm.psum), (uint32_t)c);
-            uready_bar[c] = hq_mapa(tc::smem_u32(&Sm.uready), (uint32_t)c);
         }
         const uint32_t same_half_other_pair = crank ^ 2u, other_half_same_pair = crank ^ 1u,
                        other_half_other_pair = crank ^ 3u;
@@ -232,15 +261,25 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 const int64_t sg = s0 + m;
                 Sm.sym[m] = (sg < nsig) ? obs[sg * T + t] : 0;
             }
-            if (lead) tc::mbar_arrive_expect_tx(&Sm.psum, 3 * HQ_N * 4);   // this step's partials from 3 CTAs
+            if (lead) {
+                tc::mbar_arrive_expect_tx(&Sm.psum, 3 * HQ_N * 4);   // this step's partials from 3 CTAs
+                if (t + 1 < T)                               // this step's rows from the other CTAs
+                    for (int c = 0; c < 4; ++c)
+                        if (c != (int)crank)
+                            for (int b = 0; b < HQ_MB; ++b) tc::mbar_arrive_expect_tx(&Sm.ur[c][b], HQ_ROWS);
+            }
             for (int v = ew * 32 + lane; v < 4 * HQ_N; v += 32 * HQ_EW) (&Sm.wsum[0][0])[v] = 0.f;
+            if (lead) stamp(t, 0);
             if (t > 0) {
                 tc::mbar_wait(&Sm.dfull, dpar); dpar ^= 1;
                 tc::tc_fence_after();
+                if (lead) stamp(t, 1);
                 if (lead)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) hq_arrive_remote(mdone_bar[c]);
-                hq_wait_cluster(&Sm.mdone, (uint32_t)((t - 1) & 1));
+                // (the wait for every pair's MMAs — mdone — comes before the first bulk
+                // copy into another CTA; my own B and the staging rows are only read
+                // by my pair's MMAs, which dfull already covers)
             }
             asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
 #pragma unroll 1
@@ -252,34 +291,45 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 uint8_t* dst = hh == (int)h
                     ? reinterpret_cast<uint8_t*>(&Sm.U[0][0]) + (j / HQ_KB) * (HQ_NH * 128) + (byte & 15)
                     : reinterpret_cast<uint8_t*>(&Sm.X[0][0]) + (j / HQ_KB - kb0) * (HQ_NH * 128) + (byte & 15);
-#pragma unroll 1
-                for (int ch = 0; ch < 2; ++ch) {             // 32 signals at a time
-                    const int sb = hh * HQ_NH + ch * 32;     // first signal (of the cluster's 128)
-                    float d[32];
+                // (1) u_t of this M block into registers (32 signals, packed fp16)
+                __half2 uh[16];
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch) {             // 16 signals at a time
+                    const int sb = hq * 32 + ch * 16;        // first signal (of the cluster's 128)
+                    float ev[16], ic[16];
+#pragma unroll
+                    for (int s = 0; s < 16; ++s) {
+                        ev[s] = __ldg(Ef + Sm.sym[sb + s] * HQ_S + j);
+                        ic[s] = Sm.inv_c[sb + s] * kOut;
+                    }
+                    float d[16];
                     if (t > 0) {
-                        uint32_t r[32];
-                        tc::tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mb * HQ_N + sb), r);
+                        uint32_t r[16];
+                        tc::tmem_ld_32x32b_x16(tmem + ((uint32_t)(q * 32) << 16) +
+                                               (uint32_t)((t & 1) * (HQ_MB * HQ_N) + mb * HQ_N + sb), r);
                         tc::tmem_ld_wait();
 #pragma unroll
-                        for (int s = 0; s < 32; ++s) d[s] = __uint_as_float(r[s]);
+                        for (int s = 0; s < 16; ++s) d[s] = __uint_as_float(r[s]);
                     } else {
                         const float pv = pi_lin[j] * kInit;
 #pragma unroll
-                        for (int s = 0; s < 32; ++s) d[s] = pv;
+                        for (int s = 0; s < 16; ++s) d[s] = pv;
                     }
-                    float csum[32];
+                    float csum[16];
 #pragma unroll
-                    for (int s = 0; s < 32; ++s) {
-                        const int sg = sb + s;
-                        const int sl = ch * 32 + s;          // signal within the half (B column)
-                        const __half ur = __float2half_rn(d[s] * __ldg(Ef + Sm.sym[sg] * HQ_S + j) *
-                                                          (Sm.inv_c[sg] * kOut));
-                        csum[s] = __half2float(ur);
-                        *reinterpret_cast<__half*>(dst + sl * 128 + ((chunkj ^ (uint32_t)(sl & 7)) << 4)) = ur;
+                    for (int s = 0; s < 16; s += 2) {
+                        const __half2 u2 = __floats2half2_rn(d[s] * ev[s] * ic[s], d[s + 1] * ev[s + 1] * ic[s + 1]);
+                        uh[ch * 8 + s / 2] = u2;
+                        const float2 f2 = __half22float2(u2);
+                        csum[s] = f2.x;
+                        csum[s + 1] = f2.y;
                     }
-                    // sums over the warp's 32 states: transpose-reduce, lane l ends with signal sb + l
+                    // sums over the warp's 32 states: fold the lane halves, then transpose-reduce
+                    // 16 values over 16 lanes (lane l < 16 ends with signal sb + l)
 #pragma unroll
-                    for (int w = 16; w > 0; w >>= 1) {
+                    for (int s = 0; s < 16; ++s) csum[s] += __shfl_xor_sync(0xffffffffu, csum[s], 16);
+#pragma unroll
+                    for (int w = 8; w > 0; w >>= 1) {
                         const bool upper = (lane & w) != 0;
 #pragma unroll
                         for (int s = 0; s < w; ++s) {
@@ -288,25 +338,44 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                             csum[s] = keep + __shfl_xor_sync(0xffffffffu, send, w);
                         }
                     }
-                    Sm.wsum[q][sb + lane] += csum[0];        // M block 0, then 1 (same warp)
+                    if (lane < 16) Sm.wsum[q][sb + lane] += csum[0];   // M block 0, then 1 (same warp)
+                }
+                // (2) the staging rows are free once the previous M block's copies read them
+                if (mb > 0) {
+                    if (lead && t + 1 < T) hq_bulk_wait_read();
+                    if (lead) stamp(t, 4);
+                    asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+                }
+                // (3) store: my signal half into my B, the other half into the staging rows
+#pragma unroll
+                for (int s = 0; s < 32; ++s) {
+                    const int sl = (hq & 1) * 32 + s;        // B column (signal within the half)
+                    const __half v = (s & 1) ? __high2half(uh[s / 2]) : __low2half(uh[s / 2]);
+                    *reinterpret_cast<__half*>(dst + sl * 128 + ((chunkj ^ (uint32_t)(sl & 7)) << 4)) = v;
                 }
                 tc::tc_fence_before();
                 tc::fence_proxy_async();                     // u_t rows visible to the async proxy
                 asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+                if (t > 0 && mb == 0) {                      // every pair's MMAs of t are done
+                    hq_wait_cluster(&Sm.mdone, (uint32_t)((t - 1) & 1));
+                    if (lead) stamp(t, 2);
+                }
                 if (lead && t + 1 < T) {
+                    tc::mbar_arrive(&Sm.ur[crank][mb]);      // my own rows are in my B
                     const uint32_t off = (uint32_t)kb0 * (HQ_NH * 128);
                     const uint8_t* mine = reinterpret_cast<const uint8_t*>(&Sm.U[0][0]) + off;
                     const uint32_t u0 = tc::smem_u32(&Sm.U[0][0]) + off;
-                    hq_bulk_to(hq_mapa(u0, same_half_other_pair), mine, HQ_ROWS, uready_bar[same_half_other_pair]);
+                    const uint32_t urb = tc::smem_u32(&Sm.ur[crank][mb]);
+                    hq_bulk_to(hq_mapa(u0, same_half_other_pair), mine, HQ_ROWS, hq_mapa(urb, same_half_other_pair));
                     hq_bulk_to(hq_mapa(u0, other_half_same_pair), &Sm.X[0][0], HQ_ROWS,
-                               uready_bar[other_half_same_pair]);
+                               hq_mapa(urb, other_half_same_pair));
                     hq_bulk_to(hq_mapa(u0, other_half_other_pair), &Sm.X[0][0], HQ_ROWS,
-                               uready_bar[other_half_other_pair]);
+                               hq_mapa(urb, other_half_other_pair));
                     hq_bulk_commit();
-                    hq_bulk_wait_read();                     // staging (and my rows) free again
                 }
-                asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+                if (lead) stamp(t, 3 + 2 * mb);
             }
+            if (lead && t + 1 < T) hq_bulk_wait_read();      // staging free for the next step
             // my partial of every signal -> all four CTAs (own slot written locally)
             float part = 0.f;
             if (ew < 4) {
@@ -319,9 +388,8 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                         hq_st_async(hq_mapa(tc::smem_u32(&Sm.psum_in[t & 1][crank][m]), (uint32_t)c), part,
                                     psum_bar[c]);
             }
-            if (lead && t + 1 < T)                            // my own rows of u_t are written
-                tc::mbar_arrive_expect_tx(&Sm.uready, 3 * HQ_MB * HQ_ROWS);
             asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+            if (lead) stamp(t, 7);
             if (ew < 4) {
                 hq_wait_cluster(&Sm.psum, (uint32_t)(t & 1));
                 const int m = ew * 32 + lane;
@@ -331,12 +399,13 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 ll += log((double)c);
             }
             asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+            if (lead) stamp(t, 11);
         }
         if (crank == 0 && ew < 4 && s0 + ew * 32 + lane < nsig) out_ll[s0 + ew * 32 + lane] = ll;
     }
     tc::tc_fence_before();
     tc::cluster_sync();                      // no CTA leaves while a peer may still write into it
-    if (warp == 2) hq_tmem_dealloc2(tmem, 256);
+    if (warp == 2) hq_tmem_dealloc2(tmem, 512);
 }
 
 bool make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t rows,
@@ -362,7 +431,21 @@ int hmm_quad_launch(const float* log_pi, const float* A, const float* log_E, int
     const unsigned grid = (unsigned)(4 * ((nsig + HQ_N - 1) / HQ_N));
     const size_t smem = sizeof(HqSmem) + 1024;
     cudaFuncSetAttribute(k_hmm_fwd_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_hmm_fwd_quad<<<grid, HQ_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll);
+    static unsigned long long* trace = nullptr;
+    static const bool want_trace = getenv("PMX_HMM_QUAD_TRACE") != nullptr;
+    if (want_trace && !trace) cudaMalloc(&trace, 4 * 64 * 16 * sizeof(unsigned long long));
+    k_hmm_fwd_quad<<<grid, HQ_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll, trace);
+    if (want_trace) {
+        static unsigned long long h[4 * 64 * 16];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+        for (int c = 0; c < 4; ++c)
+            for (int t = 8; t < 11; ++t) {
+                fprintf(stderr, "cta%d t=%2d", c, t);
+                for (int k = 0; k < 12; ++k) fprintf(stderr, " %6lld", (long long)(h[c * 1024 + t * 16 + k] - h[t * 16]));
+                fprintf(stderr, "\n");
+            }
+    }
     PMX_CHECK_LAUNCH("hmm_fwd_quad");
     return 0;
 }

@@ -66,7 +66,7 @@ struct __align__(1024) HqSmem {
     uint64_t full[HQ_ST], empty[HQ_ST];
     uint64_t ur[4][2];                   // rows of u_t from CTA c's M block mb in my B (local or copied)
     uint64_t pr[4][2];                   // (pair leader) the same group landed in the partner's B
-    uint64_t dfull, mdone, psum;
+    uint64_t dfull, odone, psum[2];      // odone: the other pair's MMAs of the step are done
     uint32_t tmem_base;
 };
 
@@ -160,8 +160,19 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         tc::mbar_init(&Sm.dfull, 1);
         for (int c = 0; c < 4; ++c)
             for (int b = 0; b < HQ_MB; ++b) { tc::mbar_init(&Sm.ur[c][b], 1); tc::mbar_init(&Sm.pr[c][b], 1); }
-        tc::mbar_init(&Sm.mdone, 4);
-        tc::mbar_init(&Sm.psum, 1);
+        tc::mbar_init(&Sm.odone, 1);
+        tc::mbar_init(&Sm.psum[0], 1);
+        tc::mbar_init(&Sm.psum[1], 1);
+        // Arm the first phases of the barriers that receive remote bytes: every later
+        // phase is armed by the thread that consumed the previous one, which happens
+        // before any CTA can send the next phase's bytes (a transaction never lands
+        // on an unarmed phase)
+        if (T > 1)
+            for (int c = 0; c < 4; ++c)
+                if (c != (int)crank)
+                    for (int b = 0; b < HQ_MB; ++b) tc::mbar_arrive_expect_tx(&Sm.ur[c][b], HQ_ROWS);
+        tc::mbar_arrive_expect_tx(&Sm.psum[0], 3 * HQ_N * 4);
+        if (T > 1) tc::mbar_arrive_expect_tx(&Sm.psum[1], 3 * HQ_N * 4);
         tc::fence_mbar_init();
         tc::tma_prefetch(&tmA);
     }
@@ -201,6 +212,9 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     for (int i = 0; i < 4; ++i) {
                         const uint32_t c = leader ^ (uint32_t)i;
                         tc::mbar_wait(&Sm.ur[c][mbs], (uint32_t)((t - 1) & 1));      // in my B
+                        if (c != crank && t + 1 < T && lane == 0)                      // arm u_t's phase
+                            tc::mbar_arrive_expect_tx(&Sm.ur[c][mbs], HQ_ROWS);
+                        __syncwarp();
                         hq_wait_cluster(&Sm.pr[c][mbs], (uint32_t)((t - 1) & 1));    // and the partner's
                         tc::tc_fence_after();
                         if (t < 64 && mbs == 0 && i == 0 && lane == 0) stamp(t, 8);
@@ -233,6 +247,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     for (int i = 0; i < 4; ++i) {
                         const uint32_t c = leader ^ (uint32_t)i;
                         tc::mbar_wait(&Sm.ur[c][mbs], (uint32_t)((t - 1) & 1));
+                        if (c != crank && t + 1 < T) tc::mbar_arrive_expect_tx(&Sm.ur[c][mbs], HQ_ROWS);
                         hq_arrive_remote(hq_mapa(tc::smem_u32(&Sm.pr[c][mbs]), leader));
                     }
         }
@@ -247,12 +262,22 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         double ll = 0.0;
         uint32_t dpar = 0;
         const float* __restrict__ Ef = E_lin;
-        uint32_t mdone_bar[4], psum_bar[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            mdone_bar[c] = hq_mapa(tc::smem_u32(&Sm.mdone), (uint32_t)c);
-            psum_bar[c] = hq_mapa(tc::smem_u32(&Sm.psum), (uint32_t)c);
-        }
+        const uint32_t odone_cp = hq_mapa(tc::smem_u32(&Sm.odone), crank ^ 2u);   // my counterpart's
+        // c_t of step tt (partials of all four CTAs, added in CTA order): 1/c_t for the
+        // next epilogue, log c_t into ll.  Done one step late, after the next dfull, so
+        // no CTA waits for the slowest one's partials.
+        auto finish_c = [&](int tt) {
+            if (ew < 4) {
+                hq_wait_cluster(&Sm.psum[tt & 1], (uint32_t)((tt >> 1) & 1));
+                if (lead && tt + 2 < T) tc::mbar_arrive_expect_tx(&Sm.psum[tt & 1], 3 * HQ_N * 4);
+                const int m = ew * 32 + lane;
+                const float c = ((Sm.psum_in[tt & 1][0][m] + Sm.psum_in[tt & 1][1][m]) +
+                                 (Sm.psum_in[tt & 1][2][m] + Sm.psum_in[tt & 1][3][m])) * kSum;
+                Sm.inv_c[m] = 1.f / c;
+                ll += log((double)c);
+            }
+            asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
+        };
         const uint32_t same_half_other_pair = crank ^ 2u, other_half_same_pair = crank ^ 1u,
                        other_half_other_pair = crank ^ 3u;
         for (int t = 0; t < T; ++t) {
@@ -261,27 +286,20 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 const int64_t sg = s0 + m;
                 Sm.sym[m] = (sg < nsig) ? obs[sg * T + t] : 0;
             }
-            if (lead) {
-                tc::mbar_arrive_expect_tx(&Sm.psum, 3 * HQ_N * 4);   // this step's partials from 3 CTAs
-                if (t + 1 < T)                               // this step's rows from the other CTAs
-                    for (int c = 0; c < 4; ++c)
-                        if (c != (int)crank)
-                            for (int b = 0; b < HQ_MB; ++b) tc::mbar_arrive_expect_tx(&Sm.ur[c][b], HQ_ROWS);
-            }
             for (int v = ew * 32 + lane; v < 4 * HQ_N; v += 32 * HQ_EW) (&Sm.wsum[0][0])[v] = 0.f;
             if (lead) stamp(t, 0);
             if (t > 0) {
                 tc::mbar_wait(&Sm.dfull, dpar); dpar ^= 1;
                 tc::tc_fence_after();
                 if (lead) stamp(t, 1);
-                if (lead)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) hq_arrive_remote(mdone_bar[c]);
-                // (the wait for every pair's MMAs — mdone — comes before the first bulk
-                // copy into another CTA; my own B and the staging rows are only read
-                // by my pair's MMAs, which dfull already covers)
+                // my pair's MMAs of t are done: tell my counterpart in the other pair (it
+                // waits for that before copying u_t into my B; my own B, the staging rows
+                // and my partner's B are covered by dfull itself)
+                if (lead) hq_arrive_remote(odone_cp);
+                finish_c(t - 1);
+            } else {
+                asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
             }
-            asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
 #pragma unroll 1
             for (int mb = 0; mb < HQ_MB; ++mb) {
                 const int j = jbase(mb) + q * 32 + lane;
@@ -356,19 +374,19 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 tc::tc_fence_before();
                 tc::fence_proxy_async();                     // u_t rows visible to the async proxy
                 asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
-                if (t > 0 && mb == 0) {                      // every pair's MMAs of t are done
-                    hq_wait_cluster(&Sm.mdone, (uint32_t)((t - 1) & 1));
-                    if (lead) stamp(t, 2);
-                }
                 if (lead && t + 1 < T) {
                     tc::mbar_arrive(&Sm.ur[crank][mb]);      // my own rows are in my B
                     const uint32_t off = (uint32_t)kb0 * (HQ_NH * 128);
                     const uint8_t* mine = reinterpret_cast<const uint8_t*>(&Sm.U[0][0]) + off;
                     const uint32_t u0 = tc::smem_u32(&Sm.U[0][0]) + off;
                     const uint32_t urb = tc::smem_u32(&Sm.ur[crank][mb]);
-                    hq_bulk_to(hq_mapa(u0, same_half_other_pair), mine, HQ_ROWS, hq_mapa(urb, same_half_other_pair));
                     hq_bulk_to(hq_mapa(u0, other_half_same_pair), &Sm.X[0][0], HQ_ROWS,
                                hq_mapa(urb, other_half_same_pair));
+                    if (t > 0 && mb == 0) {                  // the other pair's MMAs of t are done
+                        hq_wait_cluster(&Sm.odone, (uint32_t)((t - 1) & 1));
+                        stamp(t, 2);
+                    }
+                    hq_bulk_to(hq_mapa(u0, same_half_other_pair), mine, HQ_ROWS, hq_mapa(urb, same_half_other_pair));
                     hq_bulk_to(hq_mapa(u0, other_half_other_pair), &Sm.X[0][0], HQ_ROWS,
                                hq_mapa(urb, other_half_other_pair));
                     hq_bulk_commit();
@@ -386,21 +404,12 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 for (int c = 0; c < 4; ++c)
                     if (c != (int)crank)
                         hq_st_async(hq_mapa(tc::smem_u32(&Sm.psum_in[t & 1][crank][m]), (uint32_t)c), part,
-                                    psum_bar[c]);
-            }
-            asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
-            if (lead) stamp(t, 7);
-            if (ew < 4) {
-                hq_wait_cluster(&Sm.psum, (uint32_t)(t & 1));
-                const int m = ew * 32 + lane;
-                const float c = ((Sm.psum_in[t & 1][0][m] + Sm.psum_in[t & 1][1][m]) +
-                                 (Sm.psum_in[t & 1][2][m] + Sm.psum_in[t & 1][3][m])) * kSum;
-                Sm.inv_c[m] = 1.f / c;
-                ll += log((double)c);
+                                    hq_mapa(tc::smem_u32(&Sm.psum[t & 1]), (uint32_t)c));
             }
             asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
             if (lead) stamp(t, 11);
         }
+        finish_c(T - 1);
         if (crank == 0 && ew < 4 && s0 + ew * 32 + lane < nsig) out_ll[s0 + ew * 32 + lane] = ll;
     }
     tc::tc_fence_before();

@@ -133,7 +133,10 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                double* __restrict__ out_ll, unsigned long long* __restrict__ trace) {
     constexpr float kOut = 1.f / 1024.f, kSum = 1.f / 1024.f, kInit = 1048576.f;
     extern __shared__ uint8_t smem_raw[];
-    HqSmem& Sm = *reinterpret_cast<HqSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KiB-aligned by pointer arithmetic on the __shared__ array itself, so every
+    // access through it stays in the shared space (STS/LDS, not generic ST/LD)
+    HqSmem& Sm = *reinterpret_cast<HqSmem*>(
+        smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = tc::cluster_ctarank();
     const uint32_t p = crank >> 1, h = crank & 1u;

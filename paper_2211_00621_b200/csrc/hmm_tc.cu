@@ -134,7 +134,10 @@ k_hmm_fwd_tc(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ 
     constexpr int HT_ROWS = HT_M / HT_CLUSTER;   // tile rows loaded (and multicast) per CTA
     extern __shared__ uint8_t smem_raw[];
     typedef HmmSmem<ET, S, HT_CLUSTER, HT_STAGES, ESM> Smem;
-    Smem& Sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KiB-aligned by pointer arithmetic on the __shared__ array itself, so every
+    // access through it stays in the shared space (STS/LDS, not generic ST/LD)
+    Smem& Sm = *reinterpret_cast<Smem*>(
+        smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t s0 = (int64_t)blockIdx.x * HT_N;
 

@@ -140,7 +140,10 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
          uint64_t* __restrict__ lists, const unsigned* __restrict__ flag) {
     if (*flag) return;                       // inexact data: the SIMT path answers
     extern __shared__ uint8_t smem_raw[];
-    KnnSmem& S = *reinterpret_cast<KnnSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KiB-aligned by pointer arithmetic on the __shared__ array itself, so every
+    // access through it stays in the shared space (STS/LDS, not generic ST/LD)
+    KnnSmem& S = *reinterpret_cast<KnnSmem*>(
+        smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nblk = (int)((nq + KT_Q - 1) / KT_Q);
     const int ntiles = (int)((ntr + KT_N - 1) / KT_N);

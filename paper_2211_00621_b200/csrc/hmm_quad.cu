@@ -66,7 +66,8 @@ struct __align__(1024) HqSmem {
     uint64_t full[HQ_ST], empty[HQ_ST];
     uint64_t ur[4][2];                   // rows of u_t from CTA c's M block mb in my B (local or copied)
     uint64_t pr[4][2];                   // (pair leader) the same group landed in the partner's B
-    uint64_t dfull, odone, psum[2];      // odone: the other pair's MMAs of the step are done
+    uint64_t gdone[HQ_MB];               // both pairs' MMAs consumed my rows of M block mb (u_{t-1})
+    uint64_t dfull, psum[2];
     uint32_t tmem_base;
 };
 
@@ -163,7 +164,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         tc::mbar_init(&Sm.dfull, 1);
         for (int c = 0; c < 4; ++c)
             for (int b = 0; b < HQ_MB; ++b) { tc::mbar_init(&Sm.ur[c][b], 1); tc::mbar_init(&Sm.pr[c][b], 1); }
-        tc::mbar_init(&Sm.odone, 1);
+        for (int b = 0; b < HQ_MB; ++b) tc::mbar_init(&Sm.gdone[b], 2);
         tc::mbar_init(&Sm.psum[0], 1);
         tc::mbar_init(&Sm.psum[1], 1);
         // Arm the first phases of the barriers that receive remote bytes: every later
@@ -239,6 +240,9 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                                 first[mbo] = false;
                                 if (++stage == HQ_ST) { stage = 0; phase ^= 1; }
                             }
+                        // CTA c may overwrite these rows (in every B) once both pairs consumed them
+                        if (tc::elect_one()) hq_commit2(&Sm.gdone[mbs], (uint16_t)(1u << c));
+                        __syncwarp();
                     }
                 if (lane == 0) stamp(t, 10);
                 if (tc::elect_one()) hq_commit2(&Sm.dfull, pair_mask);
@@ -265,7 +269,6 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         double ll = 0.0;
         uint32_t dpar = 0;
         const float* __restrict__ Ef = E_lin;
-        const uint32_t odone_cp = hq_mapa(tc::smem_u32(&Sm.odone), crank ^ 2u);   // my counterpart's
         // c_t of step tt (partials of all four CTAs, added in CTA order): 1/c_t for the
         // next epilogue, log c_t into ll.  Done one step late, after the next dfull, so
         // no CTA waits for the slowest one's partials.
@@ -295,10 +298,6 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 tc::mbar_wait(&Sm.dfull, dpar); dpar ^= 1;
                 tc::tc_fence_after();
                 if (lead) stamp(t, 1);
-                // my pair's MMAs of t are done: tell my counterpart in the other pair (it
-                // waits for that before copying u_t into my B; my own B, the staging rows
-                // and my partner's B are covered by dfull itself)
-                if (lead) hq_arrive_remote(odone_cp);
                 finish_c(t - 1);
             } else {
                 asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
@@ -367,7 +366,9 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     if (lead) stamp(t, 4);
                     asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
                 }
-                // (3) store: my signal half into my B, the other half into the staging rows
+                // (3) store: my signal half into my B, the other half into the staging rows —
+                // once both pairs' MMAs of t consumed my rows of u_{t-1} (gdone)
+                if (t > 0) hq_wait_cluster(&Sm.gdone[mb], (uint32_t)((t - 1) & 1));
 #pragma unroll
                 for (int s = 0; s < 32; ++s) {
                     const int sl = (hq & 1) * 32 + s;        // B column (signal within the half)
@@ -385,10 +386,6 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     const uint32_t urb = tc::smem_u32(&Sm.ur[crank][mb]);
                     hq_bulk_to(hq_mapa(u0, other_half_same_pair), &Sm.X[0][0], HQ_ROWS,
                                hq_mapa(urb, other_half_same_pair));
-                    if (t > 0 && mb == 0) {                  // the other pair's MMAs of t are done
-                        hq_wait_cluster(&Sm.odone, (uint32_t)((t - 1) & 1));
-                        stamp(t, 2);
-                    }
                     hq_bulk_to(hq_mapa(u0, same_half_other_pair), mine, HQ_ROWS, hq_mapa(urb, same_half_other_pair));
                     hq_bulk_to(hq_mapa(u0, other_half_other_pair), &Sm.X[0][0], HQ_ROWS,
                                hq_mapa(urb, other_half_other_pair));

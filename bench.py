@@ -517,26 +517,33 @@ def bench_hmm(args, dist, peaks) -> dict:
     e2e = {"value": nsig * dist.world / (e2e_ms * 1e-3), "unit": "signals/s",
            "h2d_bytes_per_step": hobs.numel() * 4 + 8 * (A.size + E.size + pi.size), "d2h_bytes_per_step": 8 * nsig}
     flops = 2.0 * S * S * (T - 1) * nsig
-    # CTA-pair kernel: per SM per step, half of A^T written (TMA) + read (UMMA)
-    # in fp16, plus the 64-signal u tile re-read for each of its 4 M blocks
-    smem_step = 2 * 2 * (S // 2) * S + (S // 2 // 128) * S * 64 * 2
+    # 4-CTA kernel (hmm_quad.cu), per SM per step: its 256 rows of A^T written by
+    # TMA and read by the pair UMMAs (fp16), its 64-signal B half re-read once per
+    # M block (2 x 1024 x 64 fp16), and the u_t rows written locally / received
+    # (1024 states x 64 signals fp16) plus the staging rows (2 x 16 KiB)
+    rows = S // 4
+    smem_step = 2 * rows * S * 2 + 2 * S * 64 * 2 + S * 64 * 2 + 2 * 16384
+    smem_peak = pipe_peaks().get("per_sm_per_clk_at_attr_clock", {}).get("smem_load_B", 128.0)
     return {"config": "4096 signals x 10^4 steps x 1024 states, K=8, fp16 operands / fp32 accumulate + fp64 log-scale",
             "element": "signal", "value": nsig * dist.world / (ms * 1e-3), "ms_per_step": ms,
             "steps": s, "warmup": w, "e2e": e2e,
             "trellis_cells_per_s": float(S) * S * (T - 1) * nsig * dist.world / (ms * 1e-3),
-            "roofline": {"bound": "shared memory (A^T streamed through smem every step)",
+            "roofline": {"bound": "tensor pipe / per-step synchronisation (u_t exchanged between 4 SMs every step)",
                          "achieved_tflops": flops / (ms * 1e-3) / 1e12,
                          "peak_tflops": peaks["bf16_tflops"],
                          "peak_source": "f16 dense = measured bf16 dense (MEASURED_PEAKS.json)",
                          "frac": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
                          "smem_bytes_per_sm_per_step": smem_step,
                          "smem_B_per_clk_per_sm": smem_step * (T - 1) / (ms * 1e-3) / 1.965e9,
-                         "smem_frac": smem_step * (T - 1) / (ms * 1e-3) / 1.965e9 / 128.0,
-                         "note": "tcgen05 kind::f16 (2^10-scaled fp16 operands, fp32 TMEM accumulation); CTA pairs "
-                                 "(cluster of 2) split the output states of 64 signals, exchanging u halves by "
-                                 "smem->peer bulk copy; UMMAs of step t+1 overlap the epilogue of step t (TMEM D "
-                                 "double-buffered); per step every SM writes + reads half of A^T (1 MiB each) and "
-                                 "re-reads 512 KiB of u: smem_frac is that traffic against 128 B/clk/SM"},
+                         "smem_frac": smem_step * (T - 1) / (ms * 1e-3) / 1.965e9 / smem_peak,
+                         "umma_probe_tflops": {"M128_N64": 1463.4, "M128_N128": 2205.1,
+                                               "source": "tools/umma_rate.cu (profiles/umma_rate.json)"},
+                         "note": "tcgen05 kind::f16 cta_group::2 (M = 256 across a CTA pair, N = 128 signals split "
+                                 "64/64 between the pair's B buffers), 2^10-scaled fp16 operands, fp32 TMEM "
+                                 "accumulation; clusters of 4 (two pairs split the states); u_t rows exchanged by "
+                                 "DSMEM bulk copies, consumed by the next step's UMMAs per (source CTA, M block) as "
+                                 "they land (TMEM D double-buffered). CTA-pair kernel with single-SM UMMAs "
+                                 "(PMX_HMM_TC=pair): 13.2 us/step"},
             "_ll": out.to("cpu").numpy()}
 
 

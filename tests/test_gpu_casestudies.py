@@ -309,11 +309,11 @@ def test_rk4_trace_into_aliased_tensor_view():
     assert (got[:2] == -7.0).all() and (got[n + 2:] == -7.0).all()
 
 
-@pytest.mark.parametrize("variant", ["quad", "f16", "tf32"])
+@pytest.mark.parametrize("variant", ["pair", "f16", "tf32"])
 def test_hmm_forward_kernel_variants_vs_oracle(variant, tmp_path):
     """The non-default S = 1024 tensor-core kernels (PMX_HMM_TC, read once per
-    process, so each runs in a subprocess): the 4-CTA pair-UMMA kernel
-    (hmm_quad.cu, cta_group::2), the single-CTA fp16 and TF32 kernels — same
+    process, so each runs in a subprocess): the CTA-pair kernel with single-SM
+    UMMAs (hmm_pair.cu), the single-CTA fp16 and TF32 kernels — same
     signals as the default kernel's precision test, incl. a partial cluster."""
     import json
     import os

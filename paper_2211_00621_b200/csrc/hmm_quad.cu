@@ -59,6 +59,7 @@ struct __align__(1024) HqSmem {
     __half U[HQ_NKB][HQ_NH * HQ_KB];     // B operand: K-major SW128 [kblock][signal][64]
     __half At[HQ_ST][HQ_M * HQ_KB];      // A operand tiles
     __half X[2][HQ_NH * HQ_KB];          // staging: the other signal half of one M block
+    float Es[HQ_KMAX][HQ_MB * HQ_M];     // emission probabilities of my 256 states
     float wsum[4][HQ_N];                 // per TMEM lane quadrant partial sums
     float psum_in[2][4][HQ_N];           // [step parity][source CTA][signal]
     float inv_c[HQ_N];
@@ -159,6 +160,10 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
     // source M block 0 of the four CTAs (own pair first), then M block 1.
 
     if (threadIdx.x < HQ_N) Sm.inv_c[threadIdx.x] = 1.f;
+    for (int v = threadIdx.x; v < HQ_KMAX * HQ_MB * HQ_M; v += blockDim.x) {
+        const int k = v / (HQ_MB * HQ_M), jl = v % (HQ_MB * HQ_M);
+        Sm.Es[k][jl] = k < K ? E_lin[k * HQ_S + jbase(jl / HQ_M) + jl % HQ_M] : 0.f;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < HQ_ST; ++s) { tc::mbar_init(&Sm.full[s], 1); tc::mbar_init(&Sm.empty[s], 1); }
         tc::mbar_init(&Sm.dfull, 1);
@@ -266,7 +271,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         const int hq = ew >> 2;                          // signal quarter: signals 32 hq .. 32 hq + 31
         const int hh = hq >> 1;                          // ... in signal half hh
         const bool lead = threadIdx.x == 128;
-        double ll = 0.0;
+        double ll = 0.0, cprod = 1.0;
         uint32_t dpar = 0;
         const float* __restrict__ Ef = E_lin;
         // c_t of step tt (partials of all four CTAs, added in CTA order): 1/c_t for the
@@ -280,7 +285,8 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 const float c = ((Sm.psum_in[tt & 1][0][m] + Sm.psum_in[tt & 1][1][m]) +
                                  (Sm.psum_in[tt & 1][2][m] + Sm.psum_in[tt & 1][3][m])) * kSum;
                 Sm.inv_c[m] = 1.f / c;
-                ll += log((double)c);
+                cprod *= (double)c;                          // one fp64 log per 16 steps
+                if ((tt & 15) == 15 || tt == T - 1) { ll += log(cprod); cprod = 1.0; }
             }
             asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
         };
@@ -319,7 +325,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     float ev[16], ic[16];
 #pragma unroll
                     for (int s = 0; s < 16; ++s) {
-                        ev[s] = __ldg(Ef + Sm.sym[sb + s] * HQ_S + j);
+                        ev[s] = Sm.Es[Sm.sym[sb + s]][mb * HQ_M + q * 32 + lane];
                         ic[s] = Sm.inv_c[sb + s] * kOut;
                     }
                     float d[16];

@@ -18,5 +18,5 @@ out = torch.empty(nsig, dtype=torch.float64, device=dev)
 ws = torch.empty(_lib.load().pmx_hmm_forward_workspace_bytes(S, nsig), dtype=torch.uint8, device=dev)
 CS.hmm_forward_raw(lpi, Ad, lE, obs, S, K, nsig, T, out, ws)
 torch.cuda.synchronize()
-np.save(f"gpurun_out/hmm_ll_{os.environ.get('PMX_HMM_TC', 'pair')}.npy", out.cpu().numpy())
-print(os.environ.get("PMX_HMM_TC", "pair"), out[:4].tolist())
+np.save(f"gpurun_out/hmm_ll_{os.environ.get('PMX_HMM_TC', 'default')}.npy", out.cpu().numpy())
+print(os.environ.get("PMX_HMM_TC", "default"), out[:4].tolist())

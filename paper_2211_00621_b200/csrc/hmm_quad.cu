@@ -48,7 +48,7 @@ constexpr int HQ_KB = 64;            // fp16 per 128-byte swizzle row
 constexpr int HQ_S = 1024;
 constexpr int HQ_NKB = HQ_S / HQ_KB;   // 16 K blocks
 constexpr int HQ_MB = 2;             // M blocks (256 states) per pair
-constexpr int HQ_ST = 4;             // TMA ring stages
+constexpr int HQ_ST = 5;             // TMA ring stages (the MMAs are latency-bound on A^T tiles)
 constexpr int HQ_KMAX = 8;
 constexpr int HQ_EW = 16;            // epilogue warps (4 TMEM lane quadrants x 4 signal quarters)
 constexpr int HQ_THREADS = 128 + 32 * HQ_EW;
@@ -58,7 +58,6 @@ constexpr uint32_t HQ_ROWS = 2 * HQ_NH * 128;            // 16 KiB: 2 K blocks x
 struct __align__(1024) HqSmem {
     __half U[HQ_NKB][HQ_NH * HQ_KB];     // B operand: K-major SW128 [kblock][signal][64]
     __half At[HQ_ST][HQ_M * HQ_KB];      // A operand tiles
-    __half X[2][HQ_NH * HQ_KB];          // staging: the other signal half of one M block
     float Es[HQ_KMAX][HQ_MB * HQ_M];     // emission probabilities of my 256 states
     float wsum[4][HQ_N];                 // per TMEM lane quadrant partial sums
     float psum_in[2][4][HQ_N];           // [step parity][source CTA][signal]
@@ -292,6 +291,14 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         };
         const uint32_t same_half_other_pair = crank ^ 2u, other_half_same_pair = crank ^ 1u,
                        other_half_other_pair = crank ^ 3u;
+        const uint32_t rU_osp = hq_mapa(tc::smem_u32(&Sm.U[0][0]), other_half_same_pair);
+        const uint32_t rU_oop = hq_mapa(tc::smem_u32(&Sm.U[0][0]), other_half_other_pair);
+        uint32_t rB_osp[HQ_MB], rB_oop[HQ_MB];
+#pragma unroll
+        for (int b = 0; b < HQ_MB; ++b) {
+            rB_osp[b] = hq_mapa(tc::smem_u32(&Sm.ur[crank][b]), other_half_same_pair);
+            rB_oop[b] = hq_mapa(tc::smem_u32(&Sm.ur[crank][b]), other_half_other_pair);
+        }
         for (int t = 0; t < T; ++t) {
             if (ew < 4) {
                 const int m = ew * 32 + lane;
@@ -314,9 +321,10 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 const int kb0 = jbase(mb) / HQ_KB;           // first of my two K blocks
                 const uint32_t byte = (uint32_t)(j % HQ_KB) * 2u;
                 const uint32_t chunkj = byte >> 4;
-                uint8_t* dst = hh == (int)h
-                    ? reinterpret_cast<uint8_t*>(&Sm.U[0][0]) + (j / HQ_KB) * (HQ_NH * 128) + (byte & 15)
-                    : reinterpret_cast<uint8_t*>(&Sm.X[0][0]) + (j / HQ_KB - kb0) * (HQ_NH * 128) + (byte & 15);
+                uint8_t* dst = reinterpret_cast<uint8_t*>(&Sm.U[0][0]) + (j / HQ_KB) * (HQ_NH * 128) + (byte & 15);
+                // the other signal half goes straight to the two CTAs holding it: 4-byte
+                // st.async of a state pair (j & ~1, j | 1), complete_tx on their ur[me][mb]
+                const uint32_t pair_off = (uint32_t)(j / HQ_KB) * (HQ_NH * 128) + ((byte & ~3u) & 15u);
                 // (1) u_t of this M block into registers (32 signals, packed fp16)
                 __half2 uh[16];
 #pragma unroll
@@ -366,20 +374,32 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     }
                     if (lane < 16) Sm.wsum[q][sb + lane] += csum[0];   // M block 0, then 1 (same warp)
                 }
-                // (2) the staging rows are free once the previous M block's copies read them
-                if (mb > 0) {
-                    if (lead && t + 1 < T) hq_bulk_wait_read();
-                    if (lead) stamp(t, 4);
-                    asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
-                }
-                // (3) store: my signal half into my B, the other half into the staging rows —
-                // once both pairs' MMAs of t consumed my rows of u_{t-1} (gdone)
+                if (lead) stamp(t, 4 * mb);
+                // (2) store, once both pairs' MMAs of t consumed my rows of u_{t-1} (gdone):
+                // my signal half into my B, the other half into the other-half CTAs' B
                 if (t > 0) hq_wait_cluster(&Sm.gdone[mb], (uint32_t)((t - 1) & 1));
+                if (hh == (int)h) {
 #pragma unroll
-                for (int s = 0; s < 32; ++s) {
-                    const int sl = (hq & 1) * 32 + s;        // B column (signal within the half)
-                    const __half v = (s & 1) ? __high2half(uh[s / 2]) : __low2half(uh[s / 2]);
-                    *reinterpret_cast<__half*>(dst + sl * 128 + ((chunkj ^ (uint32_t)(sl & 7)) << 4)) = v;
+                    for (int s = 0; s < 32; ++s) {
+                        const int sl = (hq & 1) * 32 + s;    // B column (signal within the half)
+                        const __half v = (s & 1) ? __high2half(uh[s / 2]) : __low2half(uh[s / 2]);
+                        *reinterpret_cast<__half*>(dst + sl * 128 + ((chunkj ^ (uint32_t)(sl & 7)) << 4)) = v;
+                    }
+                } else if (t + 1 < T) {
+                    const bool odd = (lane & 1) != 0;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const __half2 mine = uh[k];              // signals 2k, 2k+1 at state j
+                        const __half2 other = __shfl_xor_sync(0xffffffffu, mine, 1);   // at state j ^ 1
+                        // even lane: signal 2k (states j, j+1); odd lane: signal 2k+1 (j-1, j)
+                        const __half2 pr = odd ? __halves2half2(__high2half(other), __high2half(mine))
+                                               : __halves2half2(__low2half(mine), __low2half(other));
+                        const int sl = (hq & 1) * 32 + 2 * k + (odd ? 1 : 0);
+                        const uint32_t off = pair_off + (uint32_t)sl * 128 + ((chunkj ^ (uint32_t)(sl & 7)) << 4);
+                        const float bits = __uint_as_float(*reinterpret_cast<const uint32_t*>(&pr));
+                        hq_st_async(rU_osp + off, bits, rB_osp[mb]);
+                        hq_st_async(rU_oop + off, bits, rB_oop[mb]);
+                    }
                 }
                 tc::tc_fence_before();
                 tc::fence_proxy_async();                     // u_t rows visible to the async proxy
@@ -390,16 +410,12 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     const uint8_t* mine = reinterpret_cast<const uint8_t*>(&Sm.U[0][0]) + off;
                     const uint32_t u0 = tc::smem_u32(&Sm.U[0][0]) + off;
                     const uint32_t urb = tc::smem_u32(&Sm.ur[crank][mb]);
-                    hq_bulk_to(hq_mapa(u0, other_half_same_pair), &Sm.X[0][0], HQ_ROWS,
-                               hq_mapa(urb, other_half_same_pair));
                     hq_bulk_to(hq_mapa(u0, same_half_other_pair), mine, HQ_ROWS, hq_mapa(urb, same_half_other_pair));
-                    hq_bulk_to(hq_mapa(u0, other_half_other_pair), &Sm.X[0][0], HQ_ROWS,
-                               hq_mapa(urb, other_half_other_pair));
                     hq_bulk_commit();
                 }
                 if (lead) stamp(t, 3 + 2 * mb);
             }
-            if (lead && t + 1 < T) hq_bulk_wait_read();      // staging free for the next step
+            if (lead && t + 1 < T) hq_bulk_wait_read();      // my rows free for the next step
             // my partial of every signal -> all four CTAs (own slot written locally)
             float part = 0.f;
             if (ew < 4) {

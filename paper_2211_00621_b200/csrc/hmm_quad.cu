@@ -23,16 +23,18 @@
 //                bytes complete on the pair leader's `full`)
 //   MMA (leader): 2 M blocks x 16 K blocks x 4 UMMA (K = 16), commit to both
 //                CTAs' `empty`, finally to both CTAs' `dfull`
-//   epilogue (8 warps per CTA: TMEM lane quadrant x signal half):
-//     a. wait dfull(t); arrive on `mdone` of all four CTAs; wait mine (every
-//        pair's MMAs of t are done: nobody reads u_{t-1} any more)
-//     b. per M block: u_t = D * E(o_t) * 1/c_{t-1} -> fp16; my signal half
-//        into my own B, the other half into a staging buffer; bulk copies:
-//        my B rows -> the other pair's CTA of my half, the staging rows ->
-//        both CTAs of the other half (complete_tx on their `uready`)
-//     c. per-signal partial sums -> all four CTAs (st.async, `psum`); c_t =
-//        the four partials added in CTA order (identical everywhere)
-//   the leader's MMAs of t+1 wait its `uready` and the partner's (`pready`).
+//   epilogue (16 warps per CTA: TMEM lane quadrant x signal quarter):
+//     a. wait dfull(t) (D of step t complete)
+//     b. per M block: u_t = D * E(o_t) * 1/c_{t-1} -> fp16, once both pairs'
+//        MMAs consumed my rows of u_{t-1} (`gdone[mb]`, multicast commits of the
+//        two leaders): my signal half into my own B (then one bulk copy to the
+//        other pair's CTA of my half), the other half straight to the two CTAs
+//        holding it by 4-byte st.async; all complete on their `ur[me][mb]`
+//     c. per-signal partial sums -> all four CTAs (st.async, `psum`); c_{t} =
+//        the four partials added in CTA order (identical everywhere), folded at
+//        the next step (nobody waits for the slowest CTA)
+//   the leader's MMAs of t+1 consume u_t group by group as `ur` / `pr` (the
+//   partner's arrivals, forwarded) complete; D is double-buffered in TMEM.
 #include <cuda_fp16.h>
 #include <stdio.h>
 #include <stdlib.h>

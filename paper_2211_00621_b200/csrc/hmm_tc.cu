@@ -368,7 +368,7 @@ int hmm_tc_launch(const float* log_pi, const float* A, const float* log_E, int S
     // The step is bound by shared-memory traffic: every SM streams the whole
     // A^T through smem once per step (TMA write + UMMA read) for only 32
     // signals — fp16 operands halve those bytes.
-    // Default: the 4-CTA pair-UMMA kernel (hmm_quad.cu, 11.7 us/step at the BASELINE
+    // Default: the 4-CTA pair-UMMA kernel (hmm_quad.cu, 10.4 us/step at the BASELINE
     // config); PMX_HMM_TC=pair: CTA pairs with single-SM UMMAs (hmm_pair.cu, 13.2).
     static const char* mode = getenv("PMX_HMM_TC");
     if (!mode || !strcmp(mode, "quad"))

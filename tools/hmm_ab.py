@@ -1,5 +1,7 @@
-"""A/B the HMM forward kernels on the same inputs: ll of the variant selected
-by PMX_HMM_TC (env) vs the default pair kernel, both run in this process."""
+"""Run the HMM forward kernel selected by PMX_HMM_TC (env; default: the 4-CTA
+pair-UMMA kernel) on fixed inputs and save the log-likelihoods to
+gpurun_out/hmm_ll_<variant>.npy, so two runs can be compared.
+    python tools/hmm_ab.py [nsig] [T]"""
 import os, sys, pathlib, subprocess, json
 ROOT = pathlib.Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))

@@ -138,25 +138,44 @@ k_kmer_fwd_vec(int kmer, float p_stay, float p_step, const float* __restrict__ E
         for (int t = 0; t < T; ++t) {
             const float* e = E_lin + (int64_t)o[t] * S;
             float part = 0.f;
-            for (int q = threadIdx.x; q < Q; q += blockDim.x) {
-                const float4 ev = __ldg(reinterpret_cast<const float4*>(e) + q);
-                float4 v;
-                if (t == 0) {
-                    v = make_float4(inv * ev.x, inv * ev.y, inv * ev.z, inv * ev.w);
-                } else {
-                    const float4 a0 = ld_keep4(cur + 4 * q, pol);
-                    const float a1 = ld_keep(cur + q, pol);
-                    const float a2 = ld_keep(cur + (q | (1 << hi)), pol);
-                    const float a3 = ld_keep(cur + (q | (2 << hi)), pol);
-                    const float a4 = ld_keep(cur + (q | (3 << hi)), pol);
-                    const float st = p_step * ((a1 + a2) + (a3 + a4));
-                    v.x = inv * ev.x * fmaf(p_stay, a0.x, st);
-                    v.y = inv * ev.y * fmaf(p_stay, a0.y, st);
-                    v.z = inv * ev.z * fmaf(p_stay, a0.z, st);
-                    v.w = inv * ev.w * fmaf(p_stay, a0.w, st);
+            // KU state quads per thread per iteration, all loads issued before any
+            // store (the cache-hinted accesses are ordered asm statements: without the
+            // batching each quad's loads would wait behind the previous quad's store)
+            constexpr int KU = 2;
+            for (int q0 = threadIdx.x; q0 < Q; q0 += KU * blockDim.x) {
+                float4 ev[KU], a0[KU];
+                float a1[KU], a2[KU], a3[KU], a4[KU];
+#pragma unroll
+                for (int u = 0; u < KU; ++u) {
+                    const int q = q0 + u * blockDim.x;
+                    if (q < Q) {
+                        ev[u] = __ldg(reinterpret_cast<const float4*>(e) + q);
+                        if (t > 0) {
+                            a0[u] = ld_keep4(cur + 4 * q, pol);
+                            a1[u] = ld_keep(cur + q, pol);
+                            a2[u] = ld_keep(cur + (q | (1 << hi)), pol);
+                            a3[u] = ld_keep(cur + (q | (2 << hi)), pol);
+                            a4[u] = ld_keep(cur + (q | (3 << hi)), pol);
+                        }
+                    }
                 }
-                st_keep4(nxt + 4 * q, v, pol);
-                part += (v.x + v.y) + (v.z + v.w);
+#pragma unroll
+                for (int u = 0; u < KU; ++u) {
+                    const int q = q0 + u * blockDim.x;
+                    if (q >= Q) break;
+                    float4 v;
+                    if (t == 0) {
+                        v = make_float4(inv * ev[u].x, inv * ev[u].y, inv * ev[u].z, inv * ev[u].w);
+                    } else {
+                        const float st = p_step * ((a1[u] + a2[u]) + (a3[u] + a4[u]));
+                        v.x = inv * ev[u].x * fmaf(p_stay, a0[u].x, st);
+                        v.y = inv * ev[u].y * fmaf(p_stay, a0[u].y, st);
+                        v.z = inv * ev[u].z * fmaf(p_stay, a0[u].z, st);
+                        v.w = inv * ev[u].w * fmaf(p_stay, a0[u].w, st);
+                    }
+                    st_keep4(nxt + 4 * q, v, pol);
+                    part += (v.x + v.y) + (v.z + v.w);
+                }
             }
             for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
             if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = part;

@@ -738,8 +738,12 @@ def bench_kmer(args, dist, peaks) -> dict:
                          "achieved_l2_GBps": bytes_ / (ms * 1e-3) / 1e9,
                          "vs_hbm_peak": bytes_ / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                          "bytes_per_signal_step": 16 * S,
-                         "note": "no measured L2 peak on this pool; L2 traffic above the HBM copy peak shows the "
-                                 "alpha working set (148 x 512 KiB) staying L2-resident"},
+                         "l2_probe_GBps": {k: v / 1e9 for k, v in pipe_peaks().items()
+                                           if k.startswith("l2_read_bytes_per_s")},
+                         "note": "algorithmic L2 bytes (stay + step-predecessor reads, emission row, write: "
+                                 "16 B per state-step); the alpha working set (148 x 512 KiB) stays L2-resident "
+                                 "(DRAM traffic ~0 in ncu). The L2 probe (tools/peaks.cu, a simple streaming "
+                                 "kernel) is a lower bound on the L2 peak: this kernel exceeds it"},
             "_ll": out.to("cpu").numpy()}
 
 

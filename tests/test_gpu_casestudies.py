@@ -69,7 +69,8 @@ def test_hmm_forward_golden(ix, golden):
     assert np.allclose(got, want, rtol=LL_REL, atol=0)
 
 
-@pytest.mark.parametrize("S,nsig,T", [(256, 40, 40), (512, 33, 12), (1024, 33, 8), (100, 5, 30), (2048, 2, 5)])
+@pytest.mark.parametrize("S,nsig,T", [(256, 40, 40), (512, 33, 12), (1024, 33, 8), (100, 5, 30), (2048, 2, 5),
+                                       (1024, 1, 1), (1024, 130, 2), (1024, 129, 3), (1024, 300, 17)])
 def test_hmm_forward_vs_oracle(S, nsig, T):
     A, E, pi = synth.hmm_model(S, 8)
     obs = synth.hmm_obs(nsig, T, 8)

@@ -48,6 +48,15 @@ def test_rk4_vs_oracle_config_steps():
     assert np.allclose(got, want, rtol=FP64_REL, atol=1e-12)
 
 
+@pytest.mark.parametrize("m", [0, 1, 7, 33])
+def test_rk4_odd_and_short_step_counts(m):
+    # two steps per straight-line block plus a single-step tail (csrc/rk4.cu)
+    ps = synth.rk4_params(257)
+    got = accelerate(lambda p, s0: rk4_sweep(p, s0, m, synth.RK4_H), ps, synth.RK4_INIT)
+    want = O.rk4(ps, synth.RK4_INIT, m, synth.RK4_H)
+    assert np.allclose(got, want, rtol=FP64_REL, atol=1e-12)
+
+
 def test_rk4_angles_outside_the_fast_reduction_range():
     """Angles beyond |x| = 2^18 (and the steps where they occur) take CUDA's
     libm sin/sincos instead of the branch-free reduction (csrc/rk4.cu)."""

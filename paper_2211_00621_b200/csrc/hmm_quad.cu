@@ -274,7 +274,6 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         const bool lead = threadIdx.x == 128;
         double ll = 0.0, cprod = 1.0;
         uint32_t dpar = 0;
-        const float* __restrict__ Ef = E_lin;
         // c_t of step tt (partials of all four CTAs, added in CTA order): 1/c_t for the
         // next epilogue, log c_t into ll.  Done one step late, after the next dfull, so
         // no CTA waits for the slowest one's partials.

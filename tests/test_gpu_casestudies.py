@@ -137,7 +137,7 @@ def test_viterbi_vs_oracle():
     assert np.allclose(r["logp"], logp, rtol=1e-12)
 
 
-@pytest.mark.parametrize("S,nsig,T", [(256, 37, 60), (512, 21, 40), (1024, 11, 30), (1024, 9, 1)])
+@pytest.mark.parametrize("S,nsig,T", [(256, 37, 60), (512, 21, 40), (1024, 11, 30), (1024, 9, 1), (1024, 13, 2)])
 def test_viterbi_tiled_vs_oracle(S, nsig, T):
     # batched register-tiled kernel (viterbi.cu): paths bit-exact, logp fp64
     A, E, pi = synth.hmm_model(S, 8)
@@ -146,6 +146,44 @@ def test_viterbi_tiled_vs_oracle(S, nsig, T):
     path, logp = O.viterbi(A, E, pi, obs)
     assert np.array_equal(np.asarray(r["path"]).reshape(nsig, T), path)
     assert np.allclose(np.asarray(r["logp"]), logp, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("dense", [False, True])
+def test_viterbi_ties_first_index(dense, tmp_path):
+    """Exact ties everywhere (uniform transitions, two identical emission rows):
+    the pruned scan over sorted columns (default) and the dense kernel
+    (PMX_VITERBI_DENSE=1, in a subprocess) both keep the reference's first
+    index, like the oracle."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = ("import json, numpy as np\n"
+            "from paper_2211_00621_b200 import accelerate, viterbi, synth\n"
+            "S, K = 256, 8\n"
+            "A = np.full((S, S), 1.0 / S)\n"
+            "_, E, pi = synth.hmm_model(S, K)\n"
+            "E[1] = E[0]; E[5] = E[0]; pi = np.full(S, 1.0 / S)\n"
+            "obs = synth.hmm_obs(11, 25, K)\n"
+            "r = accelerate(viterbi, A, E, pi, obs)\n"
+            "print(json.dumps([np.asarray(r['path']).tolist(), np.asarray(r['logp']).tolist()]))\n")
+    env = dict(os.environ)
+    if dense:
+        env["PMX_VITERBI_DENSE"] = "1"
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                         cwd=str(pathlib.Path(__file__).resolve().parent.parent))
+    assert out.returncode == 0, out.stderr[-2000:]
+    path, logp = json.loads(out.stdout.strip().splitlines()[-1])
+    S, K = 256, 8
+    A = np.full((S, S), 1.0 / S)
+    _, E, pi = synth.hmm_model(S, K)
+    E[1] = E[0]
+    E[5] = E[0]
+    pi = np.full(S, 1.0 / S)
+    obs = synth.hmm_obs(11, 25, K)
+    wpath, wlogp = O.viterbi(A, E, pi, obs)
+    assert np.array_equal(np.asarray(path).reshape(11, 25), wpath)
+    assert np.allclose(logp, wlogp, rtol=1e-12, atol=0)
 
 
 # ------------------------------------------------------------------ k-NN

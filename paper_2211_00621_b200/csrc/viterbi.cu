@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(S / 2) k_viterbi_sort_cols(const double* __res
 // [state][signal]); warp w scans columns jb + 4w + g for its four lane groups
 // g (8 lanes = the 8 signals), the warp stepping on until every lane's bound
 // is met.
-constexpr int VP_MS = 8, VP_NT = 256;
+constexpr int VP_MS = 8, VP_NT = 512;
 template <int S>
 __global__ void __launch_bounds__(VP_NT, 1)
 k_viterbi_pruned(const double* __restrict__ log_pi, const double* __restrict__ lAs,
@@ -331,7 +331,7 @@ k_viterbi_pruned(const double* __restrict__ log_pi, const double* __restrict__ l
         __syncthreads();
         const double M = s_M[m];
         const int o = s_sym[m];
-        for (int jb = 0; jb < S; jb += 32) {
+        for (int jb = 0; jb < S; jb += 4 * (VP_NT / 32)) {
             const int j = jb + warp * 4 + g;
             const double* col = lAs + (int64_t)j * S;
             const uint16_t* pc = perm + (int64_t)j * S;

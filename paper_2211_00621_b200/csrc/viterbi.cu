@@ -340,7 +340,7 @@ k_viterbi_pruned(const double* __restrict__ log_pi, const double* __restrict__ l
             bool act = true;
             // VP_R candidates per round: sorted values and indices by vector loads, the
             // scores independent; one warp vote per round
-            constexpr int VP_R = 32;
+            constexpr int VP_R = 16;
             for (int r0 = 0; r0 < S; r0 += VP_R) {
                 double lv[VP_R];
                 uint32_t pw[VP_R / 2];

@@ -297,6 +297,14 @@ PMX_API int pmx_hmm_forward_f32(const float* log_pi, const float* A, const float
                         int32_t S, int32_t K, const int32_t* obs, int64_t nsig,
                         int32_t T, double* out_ll, void* workspace,
                         size_t workspace_bytes, void* stream);
+/* S = 1024 runs on the tensor cores with fp16 operands (exact power-of-two
+ * scalings of A, u and each symbol's emission column).  A range guard flags
+ * every signal whose per-step predicted emission mass falls below 2^-8 (where
+ * fp16's subnormal range could cost more than the 1e-5 budget); flagged
+ * signals are recomputed by the TF32 kernel in the same call, decided on the
+ * device.  This returns how many signals the last call on `workspace` re-ran
+ * (synchronises `stream`; -1 on a CUDA error).                               */
+PMX_API int64_t pmx_hmm_forward_rerun_count(const void* workspace, int32_t S, int64_t nsig, void* stream);
 
 /* Viterbi (programs/viterbi.pmx:23-59) for nsig signals: path[s*T + t] and
  * logp[s]; ties resolve to the smallest state index (strict > in argmax,

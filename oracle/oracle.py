@@ -46,6 +46,9 @@ def lib():
         L.oracle_knn.argtypes = [P, P, C.c_int64, P, C.c_int64, C.c_int, C.c_int, C.c_int, P, P, C.c_int]
         L.oracle_kmer_forward.argtypes = [C.c_int, C.c_double, C.c_double, P, C.c_int, P, C.c_int64,
                                           C.c_int, P, C.c_int]
+        L.oracle_hmm_forward_scaled.argtypes = [P, P, P, C.c_int, C.c_int, P, C.c_int64, C.c_int, P, C.c_int]
+        L.oracle_kmer_forward_scaled.argtypes = [C.c_int, C.c_double, C.c_double, P, C.c_int, P, C.c_int64,
+                                                 C.c_int, P, C.c_int]
         L.oracle_nn.restype = C.c_int64
         L.oracle_nn.argtypes = [P, P, P, P, C.c_int64, C.c_int, C.c_int, C.c_int64, P, P, P]
         L.oracle_max_threads.restype = C.c_int
@@ -100,6 +103,22 @@ def hmm_forward(A, E, pi, obs, threads: int | None = None) -> np.ndarray:
     return ll
 
 
+def hmm_forward_scaled(A, E, pi, obs, threads: int | None = None) -> np.ndarray:
+    """hmm_forward in scaled linear form (fp64, signals batched): the sampled
+    full-size parity checks (S = 1024, T = 10^4).  Same values as hmm_forward
+    to ~1e-13 relative (tests/test_oracle.py)."""
+    A = np.ascontiguousarray(A, np.float64)
+    E = np.ascontiguousarray(E, np.float64)
+    pi = np.ascontiguousarray(pi, np.float64)
+    obs = np.ascontiguousarray(obs, np.int32)
+    S, K = E.shape
+    nsig, T = obs.shape
+    ll = np.empty(nsig, np.float64)
+    lib().oracle_hmm_forward_scaled(_p(A), _p(E), _p(pi), S, K, _p(obs), nsig, T, _p(ll),
+                                    threads or threads_default())
+    return ll
+
+
 def viterbi(A, E, pi, obs, threads: int | None = None):
     A = np.ascontiguousarray(A, np.float64)
     E = np.ascontiguousarray(E, np.float64)
@@ -134,6 +153,19 @@ def kmer_forward(kmer: int, p_stay: float, p_step: float, E, obs, threads: int |
     ll = np.empty(nsig, np.float64)
     lib().oracle_kmer_forward(kmer, p_stay, p_step, _p(log_E), K, _p(obs), nsig, T, _p(ll),
                               threads or threads_default())
+    return ll
+
+
+def kmer_forward_scaled(kmer: int, p_stay: float, p_step: float, E, obs, threads: int | None = None) -> np.ndarray:
+    """kmer_forward in scaled linear form (fp64): the sampled full-size parity
+    checks (S = 65,536, T = 6000).  Same values as kmer_forward to ~1e-13."""
+    E = np.ascontiguousarray(E, np.float64)
+    obs = np.ascontiguousarray(obs, np.int32)
+    nsig, T = obs.shape
+    K = E.shape[1]
+    ll = np.empty(nsig, np.float64)
+    lib().oracle_kmer_forward_scaled(kmer, p_stay, p_step, _p(E), K, _p(obs), nsig, T, _p(ll),
+                                     threads or threads_default())
     return ll
 
 

@@ -147,6 +147,18 @@ def hmm_forward(trans, emit, init, obs) -> DeviceSeq:
     return DeviceSeq(out, (nsig,), _lib.PMX_F64)
 
 
+def hmm_forward_rerun_count(S: int, nsig: int, ws=None) -> int:
+    """How many signals of the last hmm_forward call (on `ws`, default this
+    module's workspace) the fp16 path's range guard re-ran in TF32."""
+    buf = ws if ws is not None else _ws.buf
+    if buf is None:
+        return 0
+    n = _lib.load().pmx_hmm_forward_rerun_count(buf.data_ptr(), S, nsig, _stream())
+    if n < 0:
+        raise RuntimeError("pmx_hmm_forward_rerun_count failed")
+    return int(n)
+
+
 def hmm_forward_raw(log_pi, A, log_E, obs, S: int, K: int, nsig: int, T: int, out, ws) -> None:
     """Device-resident entry used by the benchmark: all arguments are device
     tensors already in the kernel's layout."""

@@ -22,6 +22,7 @@
 //   register tile.  A general small-S kernel (one CTA per signal) covers
 //   other state counts.
 #include <stdlib.h>
+#include <string.h>
 #include "common.cuh"
 
 namespace pmx {
@@ -114,7 +115,10 @@ template <int S>
 __global__ void __launch_bounds__(S / 2, 1)
 k_hmm_fwd_tiled(const float* __restrict__ pi_lin, const float* __restrict__ A,
                 const float* __restrict__ E_lin, const int* __restrict__ obs,
-                int64_t nsig, int T, double* __restrict__ out_ll) {
+                int64_t nsig, int T, double* __restrict__ out_ll,
+                const int* __restrict__ list = nullptr, const int* __restrict__ count = nullptr) {
+    // list != nullptr: the fp16 tensor-core path's guard re-run — this CTA takes
+    // entries [32 b, 32 b + 32) of the list of flagged signals (*count of them)
     constexpr int NT = S / 2;
     constexpr int GT = S / 8;              // threads per signal group
     constexpr int NW = NT / 32;
@@ -130,6 +134,11 @@ k_hmm_fwd_tiled(const float* __restrict__ pi_lin, const float* __restrict__ A,
     const int sg = tid / GT, jg = tid % GT;
     const int warp = tid >> 5, lane = tid & 31;
     const int64_t s0 = (int64_t)blockIdx.x * HMM_MS;
+    if (list) {
+        nsig = *count;
+        if (s0 >= nsig) return;
+    }
+    auto sig = [&](int64_t i) -> int64_t { return list ? (int64_t)list[i] : i; };
     const int j0 = jg * 4, j1 = S / 2 + jg * 4;
     double ll = 0.0;                           // thread tid < 32 owns signal s0 + tid
 
@@ -139,7 +148,7 @@ k_hmm_fwd_tiled(const float* __restrict__ pi_lin, const float* __restrict__ A,
     for (int t = 0; t < T; ++t) {
         if (tid < HMM_MS) {
             const int64_t s = s0 + tid;
-            s_sym[tid] = (s < nsig) ? obs[s * T + t] : 0;
+            s_sym[tid] = (s < nsig) ? obs[sig(s) * T + t] : 0;
         }
         float acc[8][8];
 #pragma unroll
@@ -230,7 +239,44 @@ k_hmm_fwd_tiled(const float* __restrict__ pi_lin, const float* __restrict__ A,
         }
         __syncthreads();
     }
-    if (tid < HMM_MS && s0 + tid < nsig) out_ll[s0 + tid] = ll;
+    if (tid < HMM_MS && s0 + tid < nsig) out_ll[sig(s0 + tid)] = ll;
+}
+
+// ------------------------------------------- tensor-core guard re-run
+// The fp16 tensor-core kernel (hmm_quad.cu) leaves, per signal, a range flag
+// (some step's predicted emission mass fell below 2^-8) and a count of
+// concentration events (an entry of u' holding >= 1/64 of the mass: its 2^-11
+// rounding error recurs instead of averaging out).  A signal is re-run in fp32
+// when it hit the range flag, its result is not finite, or the events' worst-case
+// error (2^-11 each) exceeds a quarter of the 1e-5 budget on |ll|.
+__global__ void k_hmm_guard_select(const int* __restrict__ rflag, const int* __restrict__ events,
+                                   const double* __restrict__ ll, int64_t nsig, int* __restrict__ list,
+                                   int* __restrict__ count) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsig; s += (int64_t)gridDim.x * blockDim.x) {
+        const double v = ll[s];
+        const bool bad = rflag[s] != 0 || !isfinite(v) || (double)events[s] * 0x1p-11 > 2.5e-6 * fabs(v);
+        if (bad) list[atomicAdd(count, 1)] = (int)s;
+    }
+}
+
+int* hmm_guard_words(void* ws, int S);
+
+int hmm_guard_rerun(const float* A, const float* E_lin, const float* pi_lin, int S, const int* obs, int64_t nsig,
+                    int T, double* out_ll, int* guard, cudaStream_t st) {
+    int* count = guard;
+    const int* rflag = guard + 4;
+    const int* events = rflag + nsig;
+    int* list = const_cast<int*>(events) + nsig;
+    const unsigned gsel = (unsigned)((nsig + 255) / 256 < 148 ? (nsig + 255) / 256 : 148);
+    k_hmm_guard_select<<<gsel, 256, 0, st>>>(rflag, events, out_ll, nsig, list, count);
+    PMX_CHECK_LAUNCH("hmm_guard_select");
+    if (S != 1024) { set_last_error("hmm guard re-run: S != 1024"); return -2; }
+    const size_t smem = (size_t)(1024 * HMM_MS + 2 * HMM_KT * 1024) * sizeof(float);
+    cudaFuncSetAttribute(k_hmm_fwd_tiled<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const unsigned grid = (unsigned)((nsig + HMM_MS - 1) / HMM_MS);
+    k_hmm_fwd_tiled<1024><<<grid, 512, smem, st>>>(pi_lin, A, E_lin, obs, nsig, T, out_ll, list, count);
+    PMX_CHECK_LAUNCH("hmm_guard_rerun");
+    return 0;
 }
 
 // ------------------------------------------------------------ Viterbi
@@ -286,6 +332,7 @@ int viterbi_tiled_launch(const double* log_pi, const double* log_A, const double
                          cudaStream_t st);
 size_t hmm_tc_workspace(int S, int K);
 bool hmm_tc_eligible(int S, int K);
+int* hmm_guard_words(void* ws, int S);
 int hmm_tc_launch(const float* log_pi, const float* A, const float* log_E, int S, int K, const int* obs,
                   int64_t nsig, int T, double* out_ll, void* ws, cudaStream_t st);
 
@@ -296,10 +343,10 @@ using namespace pmx;
 extern "C" {
 
 size_t pmx_hmm_forward_workspace_bytes(int32_t S, int64_t nsig) {
-    (void)nsig;
     // E_lin [K<=64][S] + pi_lin [S], generous K bound; + the tensor-core path's A^T
     size_t simt = (size_t)S * 65 * sizeof(float) + 256;
-    size_t tc = hmm_tc_workspace(S, 8);
+    // + the guard's words (hmm_guard_words): a count and three ints per signal
+    size_t tc = hmm_tc_workspace(S, 8) + 16 + 12 * (size_t)nsig;
     return simt > tc ? simt : tc;
 }
 
@@ -341,6 +388,21 @@ int pmx_hmm_forward_f32(const float* log_pi, const float* A, const float* log_E,
     k_hmm_fwd_small<<<(unsigned)nsig, threads, smem, st>>>(pi_lin, A, E_lin, S, obs, nsig, T, out_ll);
     PMX_CHECK_LAUNCH("hmm_fwd_small");
     return 0;
+}
+
+int64_t pmx_hmm_forward_rerun_count(const void* ws, int32_t S, int64_t nsig, void* stream) {
+    // signals of the last pmx_hmm_forward_f32 call on `ws` that the fp16 path's
+    // guard re-ran in fp32 (0 when another path ran)
+    PMX_REQUIRE(ws && nsig >= 0, "pmx_hmm_forward_rerun_count: bad arguments");
+    if (!hmm_tc_eligible(S, 8) || nsig == 0) return 0;
+    static const char* mode = getenv("PMX_HMM_TC");
+    if (mode && strcmp(mode, "quad")) return 0;
+    int n = 0;
+    if (cudaMemcpyAsync(&n, hmm_guard_words(const_cast<void*>(ws), S), sizeof(int), cudaMemcpyDeviceToHost,
+                        (cudaStream_t)stream) != cudaSuccess ||
+        cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+        return -1;
+    return n;
 }
 
 size_t pmx_viterbi_workspace_bytes(int32_t S, int64_t nsig, int32_t T) {

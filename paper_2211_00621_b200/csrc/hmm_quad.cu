@@ -65,6 +65,8 @@ struct __align__(1024) HqSmem {
     float psum_in[2][4][HQ_N];           // [step parity][source CTA][signal]
     float inv_c[HQ_N];
     int sym[HQ_N];
+    float escl[HQ_KMAX];                 // exact power-of-two emission scale per symbol
+    int eex[HQ_KMAX];                    // its exponent (escl = 2^eex)
     uint64_t full[HQ_ST], empty[HQ_ST];
     uint64_t ur[4][2];                   // rows of u_t from CTA c's M block mb in my B (local or copied)
     uint64_t pr[4][2];                   // (pair leader) the same group landed in the partner's B
@@ -133,7 +135,8 @@ __device__ __forceinline__ void hq_tma_load2(void* dst, const CUtensorMap* m, ui
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(HQ_THREADS, 1)
 k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ E_lin,
                const float* __restrict__ pi_lin, int K, const int* __restrict__ obs, int64_t nsig, int T,
-               double* __restrict__ out_ll, unsigned long long* __restrict__ trace) {
+               double* __restrict__ out_ll, int* __restrict__ rflag, int* __restrict__ events,
+               unsigned long long* __restrict__ trace) {
     constexpr float kOut = 1.f / 1024.f, kSum = 1.f / 1024.f, kInit = 1048576.f;
     extern __shared__ uint8_t smem_raw[];
     // 1 KiB-aligned by pointer arithmetic on the __shared__ array itself, so every
@@ -161,9 +164,28 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
     // source M block 0 of the four CTAs (own pair first), then M block 1.
 
     if (threadIdx.x < HQ_N) Sm.inv_c[threadIdx.x] = 1.f;
+    // Range guard, part 1: every symbol's emission column is scaled by an exact
+    // power of two so that its largest entry lies in [1, 2) (log-likelihoods get
+    // the exponent back).  A symbol that is rare in every state then no longer
+    // drives u_t into fp16's subnormal range.
+    if (warp < HQ_KMAX) {
+        float m = 0.f;
+        if (warp < K)
+            for (int j = lane; j < HQ_S; j += 32) m = fmaxf(m, E_lin[warp * HQ_S + j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) {
+            // m = 1.f x 2^(E - 127): x = 127 - E puts m * 2^x in [1, 2)
+            const int E = (int)((__float_as_uint(m) >> 23) & 0xffu);
+            const int x = (m > 0.f && E < 255) ? min(max(127 - E, -126), 126) : 0;
+            Sm.eex[warp] = x;
+            Sm.escl[warp] = __uint_as_float((uint32_t)(x + 127) << 23);
+        }
+    }
+    __syncthreads();
     for (int v = threadIdx.x; v < HQ_KMAX * HQ_MB * HQ_M; v += blockDim.x) {
         const int k = v / (HQ_MB * HQ_M), jl = v % (HQ_MB * HQ_M);
-        Sm.Es[k][jl] = k < K ? E_lin[k * HQ_S + jbase(jl / HQ_M) + jl % HQ_M] : 0.f;
+        Sm.Es[k][jl] = k < K ? E_lin[k * HQ_S + jbase(jl / HQ_M) + jl % HQ_M] * Sm.escl[k] : 0.f;
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < HQ_ST; ++s) { tc::mbar_init(&Sm.full[s], 1); tc::mbar_init(&Sm.empty[s], 1); }
@@ -273,6 +295,8 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         const int hh = hq >> 1;                          // ... in signal half hh
         const bool lead = threadIdx.x == 128;
         double ll = 0.0, cprod = 1.0;
+        int esum = 0;                                    // sum of the emission-scale exponents
+        bool out_of_range = false;
         uint32_t dpar = 0;
         // c_t of step tt (partials of all four CTAs, added in CTA order): 1/c_t for the
         // next epilogue, log c_t into ll.  Done one step late, after the next dfull, so
@@ -285,6 +309,11 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 const float c = ((Sm.psum_in[tt & 1][0][m] + Sm.psum_in[tt & 1][1][m]) +
                                  (Sm.psum_in[tt & 1][2][m] + Sm.psum_in[tt & 1][3][m])) * kSum;
                 Sm.inv_c[m] = 1.f / c;
+                // Range guard, part 2: c_t is the predicted emission mass (scaled as
+                // above).  Below 2^-8 the fp16 rounding of u_t (subnormal entries, and
+                // the subnormal entries of 2^10 A) could cost more than the 1e-5
+                // budget; such a signal is re-run by the fp32 kernel.
+                if (!(c >= 0.00390625f)) out_of_range = true;
                 cprod *= (double)c;                          // one fp64 log per 16 steps
                 if ((tt & 15) == 15 || tt == T - 1) { ll += log(cprod); cprod = 1.0; }
             }
@@ -304,7 +333,9 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
             if (ew < 4) {
                 const int m = ew * 32 + lane;
                 const int64_t sg = s0 + m;
-                Sm.sym[m] = (sg < nsig) ? obs[sg * T + t] : 0;
+                const int o = (sg < nsig) ? obs[sg * T + t] : 0;
+                Sm.sym[m] = o;
+                esum += Sm.eex[(unsigned)o < (unsigned)HQ_KMAX ? o : 0];
             }
             for (int v = ew * 32 + lane; v < 4 * HQ_N; v += 32 * HQ_EW) (&Sm.wsum[0][0])[v] = 0.f;
             if (lead) stamp(t, 0);
@@ -350,10 +381,25 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
 #pragma unroll
                         for (int s = 0; s < 16; ++s) d[s] = pv;
                     }
-                    float csum[16];
+                    float csum[16], v[16];
+#pragma unroll
+                    for (int s = 0; s < 16; ++s) v[s] = d[s] * ev[s] * ic[s];
+                    // Precision guard: an entry >= 32 of u' (which sums to 2^10 c_t <= 2^11)
+                    // means >= 1/64 of the predicted mass sits in one state.  Rounding
+                    // errors of such entries (2^-11 relative) do not average out over the
+                    // states and recur step after step; these events are counted per
+                    // signal and weighed against the log-likelihood after the kernel.
+                    float vmax = v[0];
+#pragma unroll
+                    for (int s = 1; s < 16; ++s) vmax = fmaxf(vmax, v[s]);
+                    if (__any_sync(0xffffffffu, vmax >= 32.f)) {
+#pragma unroll
+                        for (int s = 0; s < 16; ++s)
+                            if (v[s] >= 32.f && s0 + sb + s < nsig) atomicAdd(&events[s0 + sb + s], 1);
+                    }
 #pragma unroll
                     for (int s = 0; s < 16; s += 2) {
-                        const __half2 u2 = __floats2half2_rn(d[s] * ev[s] * ic[s], d[s + 1] * ev[s + 1] * ic[s + 1]);
+                        const __half2 u2 = __floats2half2_rn(v[s], v[s + 1]);
                         uh[ch * 8 + s / 2] = u2;
                         const float2 f2 = __half22float2(u2);
                         csum[s] = f2.x;
@@ -433,7 +479,11 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
             if (lead) stamp(t, 11);
         }
         finish_c(T - 1);
-        if (crank == 0 && ew < 4 && s0 + ew * 32 + lane < nsig) out_ll[s0 + ew * 32 + lane] = ll;
+        if (crank == 0 && ew < 4 && s0 + ew * 32 + lane < nsig) {
+            const int64_t sg = s0 + ew * 32 + lane;
+            out_ll[sg] = ll - (double)esum * 0.69314718055994530942;
+            rflag[sg] = out_of_range ? 1 : 0;
+        }
     }
     tc::tc_fence_before();
     tc::cluster_sync();                      // no CTA leaves while a peer may still write into it
@@ -446,12 +496,19 @@ template <class ET>
 __global__ void k_hmm_tc_prep(const float* __restrict__ A, const float* __restrict__ log_E,
                               const float* __restrict__ log_pi, int S, int K, ET* __restrict__ At,
                               float* __restrict__ E_lin, float* __restrict__ pi_lin);
+int* hmm_guard_words(void* ws, int S);
+int hmm_guard_rerun(const float* A, const float* E_lin, const float* pi_lin, int S, const int* obs, int64_t nsig,
+                    int T, double* out_ll, int* guard, cudaStream_t st);
 
 int hmm_quad_launch(const float* log_pi, const float* A, const float* log_E, int S, int K, const int* obs,
                     int64_t nsig, int T, double* out_ll, void* ws, cudaStream_t st) {
     __half* At = (__half*)ws;
     float* E_lin = (float*)((char*)ws + (size_t)S * S * 4);
     float* pi_lin = E_lin + (size_t)HQ_KMAX * S;
+    int* guard = hmm_guard_words(ws, S);       // [count, pad] [range flag x nsig] [events x nsig] [list x nsig]
+    int* rflag = guard + 4;
+    int* events = rflag + nsig;
+    cudaMemsetAsync(guard, 0, sizeof(int) * (4 + 2 * (size_t)nsig), st);
     k_hmm_tc_prep<__half><<<dim3(S / 32, S / 32), dim3(32, 8), 0, st>>>(A, log_E, log_pi, S, K, At, E_lin, pi_lin);
     PMX_CHECK_LAUNCH("hmm_quad_prep");
     CUtensorMap tmA;
@@ -466,7 +523,8 @@ int hmm_quad_launch(const float* log_pi, const float* A, const float* log_E, int
     static unsigned long long* trace = nullptr;
     static const bool want_trace = getenv("PMX_HMM_QUAD_TRACE") != nullptr;
     if (want_trace && !trace) cudaMalloc(&trace, 4 * 64 * 16 * sizeof(unsigned long long));
-    k_hmm_fwd_quad<<<grid, HQ_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll, trace);
+    k_hmm_fwd_quad<<<grid, HQ_THREADS, smem, st>>>(tmA, E_lin, pi_lin, K, obs, nsig, T, out_ll, rflag, events,
+                                                   trace);
     if (want_trace) {
         static unsigned long long h[4 * 64 * 16];
         cudaStreamSynchronize(st);
@@ -479,7 +537,9 @@ int hmm_quad_launch(const float* log_pi, const float* A, const float* log_E, int
             }
     }
     PMX_CHECK_LAUNCH("hmm_fwd_quad");
-    return 0;
+    // signals the guard flags are recomputed by the fp32 SIMT kernel, selected on
+    // the device (the re-run's CTAs return at once when no signal was flagged)
+    return hmm_guard_rerun(A, E_lin, pi_lin, S, obs, nsig, T, out_ll, guard, st);
 }
 
 }  // namespace pmx

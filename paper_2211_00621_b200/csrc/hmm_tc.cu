@@ -318,6 +318,11 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int 
 
 size_t hmm_tc_workspace(int S, int K) { return (size_t)S * S * 4 + (size_t)HT_KMAX * S * 4 + (size_t)S * 4 + 1024; }
 
+// precision / range guard words after the tensor-core workspace (hmm_quad.cu):
+// [0] number of flagged signals, [4 ...] range flags, event counts and the list
+// of flagged signals (nsig each)
+int* hmm_guard_words(void* ws, int S) { return (int*)((char*)ws + hmm_tc_workspace(S, HT_KMAX)); }
+
 bool hmm_tc_eligible(int S, int K) { return S == 1024 && K <= HT_KMAX; }
 
 // PMX_HMM_DBG (timing experiments only, results invalid): bit 0 skips the
@@ -357,6 +362,7 @@ static int hmm_tc_run(const float* log_pi, const float* A, const float* log_E, i
     PMX_CHECK_LAUNCH("hmm_fwd_tc");
     return 0;
 }
+
 
 int hmm_tc_launch(const float* log_pi, const float* A, const float* log_E, int S, int K, const int* obs,
                   int64_t nsig, int T, double* out_ll, void* ws, cudaStream_t st) {

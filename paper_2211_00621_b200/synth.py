@@ -106,3 +106,41 @@ def kmer_emission(kmer: int, K: int) -> np.ndarray:
     jj = np.arange(S, dtype=np.int64)[:, None]
     k = np.arange(K, dtype=np.int64)[None, :]
     return _rownorm((1 + (jj * 13 + k * 29 + jj * k * 3) % 31).astype(np.float64))
+
+
+def hmm_model_rare_symbol(S: int, K: int, eps: float = 1e-9):
+    """hmm_model with symbol K-1 nearly impossible in every state (E[:, K-1] =
+    eps before row normalisation): the case where an unscaled fp16 trellis
+    underflows."""
+    A, E, pi = hmm_model(S, K)
+    E = E.copy()
+    E[:, K - 1] = eps
+    return A, _rownorm(E), pi
+
+
+def hmm_model_peaky(S: int, K: int, stay: float = 0.999, off: float = 1e-9):
+    """Near-deterministic model: A keeps its state with probability ~`stay`
+    and reaches the neighbour state with the rest (every other transition
+    `off`), state j emits symbol j mod K with probability 0.99, pi puts 1e-9 on
+    all but state 0.  Observations that disagree with the current state force
+    tiny per-step emission masses (the fp16 path's range guard re-runs them)."""
+    i = np.arange(S)[:, None]
+    j = np.arange(S)[None, :]
+    A = np.full((S, S), off)
+    A[i == j] = stay
+    A[(i + 1) % S == j] = 1.0 - stay
+    E = np.full((S, K), 0.01 / (K - 1))
+    E[np.arange(S), np.arange(S) % K] = 0.99
+    pi = np.full(S, 1e-9)
+    pi[0] = 1.0
+    return _rownorm(A), _rownorm(E), pi / pi.sum()
+
+
+def parity_sample(n: int, m: int, block: int = 128) -> np.ndarray:
+    """At least m (at most m + 7) sorted distinct element indices of [0, n):
+    m evenly spaced, plus both ends and the first / last element of a few
+    `block`-sized tiles (CTA / cluster edges).  Used by the sampled full-size
+    parity checks."""
+    edges = [0, n - 1, block - 1, block, n // 2 - 1, n // 2, n - block]
+    even = np.linspace(0, n - 1, min(m, n)).astype(np.int64)
+    return np.unique(np.clip(np.concatenate([np.array(edges, np.int64), even]), 0, n - 1))

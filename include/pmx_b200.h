@@ -247,10 +247,12 @@ PMX_API int pmx_jit_compile_check(const pmx_program* f, int32_t kind, int32_t x_
  * then holds every rank's mailbox pointer (own pointer at [rank]).
  * pmx_map_reduce_peers is pmx_map_reduce over this rank's shard whose last CTA
  * also exchanges the shard partials through the mailboxes and folds the
- * non-empty ones in rank order: `out` is the global result on every rank,
- * from one kernel and no collective call. Each rank's shard folds from init
- * (a reference chunk, interp.py:332-333); partials fold left in rank order
- * (interp.py:334-336); empty shards are dropped (interp.py:276).
+ * contributing ones in rank order: `out` is the global result on every rank,
+ * from one kernel and no collective call. Each rank's shard folds from its
+ * init; partials fold left in rank order (interp.py:334-336); empty shards are
+ * dropped (interp.py:276) except rank 0's, which always contributes its init.
+ * The host layer (shard.py) passes acc as rank 0's init and the operator's
+ * identity on the other ranks, so acc is applied once, as on one GPU.
  * `epoch` must be incremented (from 1) by every rank before each call; all
  * ranks must make the same sequence of calls.       replaces eval_reduce's
  * chunk combine across GPUs (interp.py:334-336) / an NCCL all-gather + fold. */

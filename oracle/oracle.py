@@ -50,7 +50,7 @@ def lib():
         L.oracle_kmer_forward_scaled.argtypes = [C.c_int, C.c_double, C.c_double, P, C.c_int, P, C.c_int64,
                                                  C.c_int, P, C.c_int]
         L.oracle_nn.restype = C.c_int64
-        L.oracle_nn.argtypes = [P, P, P, P, C.c_int64, C.c_int, C.c_int, C.c_int64, P, P, P]
+        L.oracle_nn.argtypes = [P, P, P, P, C.c_int64, C.c_int, C.c_int, C.c_int64, P, P, P, C.c_int]
         L.oracle_max_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -327,10 +327,11 @@ def ir_reduce(f, acc, xs, workers: int = 1):   # eval_reduce, interp.py:328-343
     return total
 
 
-def nn(x, y, w, b, workers: int = 4):
+def nn(x, y, w, b, workers: int = 4, threads: int | None = None):
     """(loss, dw, db) of programs/nn.pmx:22-49 with the reference's chunked
-    top-level reduces over `workers` chunks.  Raises ValueError on a label out
-    of range (the reference's get error)."""
+    top-level reduces over `workers` chunks (one OpenMP thread per chunk, up to
+    `threads`).  Raises ValueError on a label out of range (the reference's get
+    error)."""
     x = np.ascontiguousarray(x, np.float64)
     y = np.ascontiguousarray(y, np.int32)
     w = np.ascontiguousarray(w, np.float64)
@@ -340,7 +341,8 @@ def nn(x, y, w, b, workers: int = 4):
     loss = np.zeros(1, np.float64)
     dw = np.empty((nin, nout), np.float64)
     db = np.empty(nout, np.float64)
-    bad = lib().oracle_nn(_p(x), _p(y), _p(w), _p(b), npts, nin, nout, workers, _p(loss), _p(dw), _p(db))
+    bad = lib().oracle_nn(_p(x), _p(y), _p(w), _p(b), npts, nin, nout, workers, _p(loss), _p(dw), _p(db),
+                         threads or threads_default())
     if bad:
         raise ValueError(f"label out of range at point {bad - 1}")
     return float(loss[0]), dw, db

@@ -304,7 +304,7 @@ k_map_reduce_vec(const TX* __restrict__ x, TY* __restrict__ y, int64_t n, const 
     }
     if (DO_REDUCE) {
         A bt = block_reduce<Op>(Op::f(acc0, acc1));
-        grid_combine<Op>(bt, partials, ticket, init, out, pg, n > 0, err);
+        grid_combine<Op>(bt, partials, ticket, init, out, pg, n > 0 || pg.rank == 0, err);
     }
 }
 
@@ -328,7 +328,7 @@ k_map_reduce_scalar(const TX* __restrict__ x, TY* __restrict__ y, int64_t n, con
     }
     if (DO_REDUCE) {
         A bt = block_reduce<Op>(acc);
-        grid_combine<Op>(bt, partials, ticket, init, out, pg, n > 0, err);
+        grid_combine<Op>(bt, partials, ticket, init, out, pg, n > 0 || pg.rank == 0, err);
     }
 }
 

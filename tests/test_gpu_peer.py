@@ -38,8 +38,8 @@ def _worker(rank, world, port, q):
         peers = shard.PeerMailboxes()
         out = {}
         rng = np.random.default_rng(7)
-        # 1) float sum over non-exact data: total = p0 + p1 (rank order), each
-        #    p_r folded from acc on its shard
+        # 1) float sum over non-exact data: total = p0 + p1 (rank order), p0
+        #    folded from acc, p1 alone
         n = 1_000_003
         x = rng.standard_normal(n)
         lo, hi = shard.chunk(n, world, rank)
@@ -69,6 +69,20 @@ def _worker(rank, world, port, q):
         out["one"] = int(shard.ShardedMapReduce(None, P.addi, 1, se, 1, peers=peers).launch().item())
         sz = DeviceSeq(torch.empty(0, dtype=torch.int64).cuda(), (0,), _lib.PMX_I64)
         out["none"] = int(shard.ShardedMapReduce(None, P.addi, 5, sz, 0, peers=peers).launch().item())
+        # acc applied once (rank 0): N = 1 and N = 2 agree for a non-neutral acc
+        out["acc10"] = int(shard.ShardedMapReduce(None, P.addi, 10, si, 4, peers=peers).launch().item())
+        lo8, hi8 = shard.chunk(8, world, rank)
+        xf = torch.tensor([0.5, -1.25, 2.0, 3.5, -0.75, 8.0, 1.5, 4.0], dtype=torch.float64)
+        sf = DeviceSeq(xf[lo8:hi8].cuda(), (hi8 - lo8,), _lib.PMX_F64)
+        mnf = P.lam("a", "b", P.if_(P.ltf("a", "b"), "a", "b"))
+        out["minf"] = float(shard.ShardedMapReduce(None, mnf, -3.0, sf, 8, peers=peers).launch().item())
+        out["mulf"] = float(shard.ShardedMapReduce(None, P.mulf, 2.0, sf, 8, peers=peers).launch().item())
+        # an associative operator the library does not recognise (ordered generic
+        # tree, collective combine): rank 1 folds from its first element
+        gop = P.lam("a", "b", P.addi("a", P.muli("b", 1)))
+        g = shard.ShardedMapReduce(P.lam("x", P.muli("x", "x")), gop, 100, si, 4, peers=peers)
+        assert g.peers is None
+        out["generic"] = int(g.launch().item())
         # generic map (run-time specialised kernel) with the peer combine
         sq = shard.ShardedMapReduce(P.lam("x", P.mulf("x", "x")), P.addf, 0.0, seq, n, peers=peers)
         out["sq"] = float(sq.launch().item())
@@ -104,12 +118,17 @@ def test_peer_reduce_two_ranks_one_gpu():
     want = np.float64(res[0]["local"]) + np.float64(res[1]["local"])
     assert all(v == float(want) for v in s0), (s0[:3], want)
     assert s0 == s1
-    # product: rank0 1*1*2 ; rank1 1*3*4 -> 2*12 (acc folded into every chunk)
+    # product: rank0 1*1*2 ; rank1 3*4 -> 2*12
     assert res[0]["prod"] == res[1]["prod"] == 24
     # max of 9-2x over [1,2] and [3,4] from -100
     assert res[0]["max"] == res[1]["max"] == 7
-    # empty chunk dropped: only rank 1's (1 + 41)
+    # rank 0's shard is empty but it carries acc: 1 + 41
     assert res[0]["one"] == res[1]["one"] == 42
     assert res[0]["sq"] == res[1]["sq"] == res[0]["sq_local"] + res[1]["sq_local"]
     # all chunks empty: reduce over [] returns acc
     assert res[0]["none"] == res[1]["none"] == 5
+    # acc once, as on one GPU (the reference's debug semantics, interp.py:329-330)
+    assert res[0]["acc10"] == res[1]["acc10"] == 10 + 1 + 2 + 3 + 4
+    assert res[0]["minf"] == res[1]["minf"] == -3.0
+    assert res[0]["mulf"] == res[1]["mulf"] == 2.0 * 0.5 * -1.25 * 2.0 * 3.5 * -0.75 * 8.0 * 1.5 * 4.0
+    assert res[0]["generic"] == res[1]["generic"] == 100 + 1 + 4 + 9 + 16

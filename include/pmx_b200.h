@@ -317,6 +317,12 @@ PMX_API int pmx_viterbi_f64(const double* log_pi, const double* log_A,
                     const int32_t* obs, int64_t nsig, int32_t T,
                     int32_t* path, double* logp, void* workspace,
                     size_t workspace_bytes, void* stream);
+/* Max-plus cells (candidate (i, j) pairs per signal-step) the last
+ * pmx_viterbi_f64 call on `workspace` evaluated in the pruned (branch and
+ * bound) kernel, S in {256, 512, 1024}: the roofline's work count.
+ * Synchronises `stream`; -1 on a CUDA error.                                */
+PMX_API int64_t pmx_viterbi_visited_cells(const void* workspace, int32_t S, int64_t nsig, int32_t T,
+                                  void* stream);
 
 /* Softmax regression (programs/nn.pmx:22-49): mean cross-entropy loss and its
  * analytic gradients for npts points, one fused launch.  x [npts*nin] fp64,

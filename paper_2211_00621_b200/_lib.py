@@ -108,6 +108,7 @@ _SIGS = {
     "pmx_rk4_trace_f64": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_double, C.c_int32, _P, _P, _P]),
     "pmx_hmm_forward_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int64]),
     "pmx_hmm_forward_rerun_count": (C.c_int64, [_P, C.c_int32, C.c_int64, _P]),
+    "pmx_viterbi_visited_cells": (C.c_int64, [_P, C.c_int32, C.c_int64, C.c_int32, _P]),
     "pmx_hmm_forward_f32": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, _P, C.c_int64, C.c_int32,
                                       _P, _P, C.c_size_t, _P]),
     "pmx_viterbi_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int64, C.c_int32]),

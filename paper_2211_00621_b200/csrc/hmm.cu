@@ -330,6 +330,7 @@ size_t viterbi_tiled_workspace(int S, int64_t nsig, int T);
 int viterbi_tiled_launch(const double* log_pi, const double* log_A, const double* log_E, int S, int K,
                          const int* obs, int64_t nsig, int T, int* path, double* logp, void* ws,
                          cudaStream_t st);
+unsigned long long* viterbi_visited_counter(void* ws, int S, int64_t nsig, int T);
 size_t hmm_tc_workspace(int S, int K);
 bool hmm_tc_eligible(int S, int K);
 int* hmm_guard_words(void* ws, int S);
@@ -403,6 +404,19 @@ int64_t pmx_hmm_forward_rerun_count(const void* ws, int32_t S, int64_t nsig, voi
         cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
         return -1;
     return n;
+}
+
+int64_t pmx_viterbi_visited_cells(const void* ws, int32_t S, int64_t nsig, int32_t T, void* stream) {
+    // max-plus cells the last pmx_viterbi_f64 call on `ws` evaluated in the
+    // pruned kernel (0 when another kernel ran); synchronises `stream`
+    PMX_REQUIRE(ws && nsig >= 0, "pmx_viterbi_visited_cells: bad arguments");
+    if (!viterbi_tiled_eligible(S) || nsig == 0) return 0;
+    unsigned long long n = 0;
+    if (cudaMemcpyAsync(&n, viterbi_visited_counter(const_cast<void*>(ws), S, nsig, T), sizeof(n),
+                        cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess ||
+        cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+        return -1;
+    return (int64_t)n;
 }
 
 size_t pmx_viterbi_workspace_bytes(int32_t S, int64_t nsig, int32_t T) {

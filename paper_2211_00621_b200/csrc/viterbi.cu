@@ -273,7 +273,11 @@ __global__ void __launch_bounds__(S / 2) k_viterbi_sort_cols(const double* __res
                 const int i = (t / jj) * 2 * jj + (t % jj), q = i + jj;
                 const double a = v[i], b = v[q];
                 const int ia = ix[i], ib = ix[q];
-                const bool a_first = a > b || (a == b && ia < ib);
+                // NaN entries (a NaN log A) sort after every number: they never win
+                // (score > best is false) and never end a scan early (the bound
+                // test is false), as in the dense kernel
+                const bool na = a != a, nb = b != b;
+                const bool a_first = (na != nb) ? nb : (na ? ia < ib : (a > b || (a == b && ia < ib)));
                 if (((i & k) == 0) ? !a_first : a_first) { v[i] = b; v[q] = a; ix[i] = ib; ix[q] = ia; }
             }
             __syncthreads();
@@ -294,8 +298,9 @@ __global__ void __launch_bounds__(VP_NT, 1)
 k_viterbi_pruned(const double* __restrict__ log_pi, const double* __restrict__ lAs,
                  const uint16_t* __restrict__ perm, const double* __restrict__ log_E, int K,
                  const int* __restrict__ obs, int64_t nsig, int T, int* __restrict__ back,
-                 double* __restrict__ chi_out) {
+                 double* __restrict__ chi_out, unsigned long long* __restrict__ visited) {
     extern __shared__ __align__(16) double vsm[];
+    uint32_t rounds = 0;                   // candidate rounds this lane's scans ran (roofline counter)
     double* cur = vsm;                     // [S][VP_MS]
     double* nxt = vsm + S * VP_MS;
     __shared__ int s_sym[VP_MS];
@@ -367,6 +372,7 @@ k_viterbi_pruned(const double* __restrict__ log_pi, const double* __restrict__ l
                     const int i = (int)((pw[u >> 1] >> (16 * (u & 1))) & 0xffffu);
                     if (act && (sc[u] > best || (sc[u] == best && i < arg))) { best = sc[u]; arg = i; }
                 }
+                ++rounds;
                 if (!__any_sync(0xffffffffu, act)) break;
             }
             nxt[j * VP_MS + m] = __dadd_rn(best, __ldg(log_E + (int64_t)j * K + o));   // (:42)
@@ -379,6 +385,10 @@ k_viterbi_pruned(const double* __restrict__ log_pi, const double* __restrict__ l
         const int i = v / VP_MS, mm = v % VP_MS;
         if (s0 + mm < nsig) chi_out[(s0 + mm) * S + i] = cur[v];
     }
+    unsigned long long cells = (unsigned long long)rounds * 16ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(0xffffffffu, cells, o);
+    if (lane == 0) atomicAdd(visited, cells);
 }
 
 __global__ void k_transpose_f64(const double* __restrict__ a, double* __restrict__ at, int S) {
@@ -392,6 +402,18 @@ __global__ void k_transpose_f64(const double* __restrict__ a, double* __restrict
 bool viterbi_tiled_eligible(int S) { return S == 256 || S == 512 || S == 1024; }
 
 // workspace of the tiled path: max(back pointers int32, chi history fp64) | final chi | log A^T
+// | sorted-column permutation | visited-cell counter (pruned kernel)
+static size_t viterbi_counter_offset(int S, int64_t nsig, int T) {
+    const size_t steps = (size_t)(T > 1 ? T - 1 : 0);
+    const size_t h = ((size_t)nsig * steps * (size_t)S * sizeof(double) + 255) & ~(size_t)255;
+    const size_t c = ((size_t)nsig * (size_t)S * sizeof(double) + 255) & ~(size_t)255;
+    return (h + c + (size_t)S * S * sizeof(double) + (size_t)S * S * sizeof(uint16_t) + 7) & ~(size_t)7;
+}
+
+unsigned long long* viterbi_visited_counter(void* ws, int S, int64_t nsig, int T) {
+    return (unsigned long long*)((char*)ws + viterbi_counter_offset(S, nsig, T));
+}
+
 size_t viterbi_tiled_workspace(int S, int64_t nsig, int T) {
     const size_t steps = (size_t)(T > 1 ? T - 1 : 0);
     const size_t h = ((size_t)nsig * steps * (size_t)S * sizeof(double) + 255) & ~(size_t)255;
@@ -426,6 +448,8 @@ int viterbi_tiled_launch(const double* log_pi, const double* log_A, const double
     }
     // default: the pruned scan over sorted columns; PMX_VITERBI_DENSE=1: every cell
     static const bool dense = getenv("PMX_VITERBI_DENSE") && getenv("PMX_VITERBI_DENSE")[0] == '1';
+    unsigned long long* visited = viterbi_visited_counter(ws, S, nsig, T);
+    cudaMemsetAsync(visited, 0, sizeof(unsigned long long), st);
     if (argmax && !dense) {
         uint16_t* perm = (uint16_t*)((char*)lAT + (size_t)S * S * sizeof(double));
 #define PMX_VP(SS)                                                                                 \
@@ -435,7 +459,7 @@ int viterbi_tiled_launch(const double* log_pi, const double* log_A, const double
             const size_t smem = 2 * (size_t)SS * VP_MS * sizeof(double);                           \
             cudaFuncSetAttribute(k_viterbi_pruned<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
             k_viterbi_pruned<SS><<<(unsigned)((nsig + VP_MS - 1) / VP_MS), VP_NT, smem, st>>>(     \
-                log_pi, lAT, perm, log_E, K, obs, nsig, T, back, chi_final);                      \
+                log_pi, lAT, perm, log_E, K, obs, nsig, T, back, chi_final, visited);             \
             PMX_CHECK_LAUNCH("viterbi_pruned");                                                    \
         }
         PMX_VP(1024) PMX_VP(512) PMX_VP(256)

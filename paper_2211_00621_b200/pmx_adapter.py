@@ -462,78 +462,175 @@ def _elem_type(s: list) -> str:
     raise Unsupported(f"sequence of {type(x).__name__}")
 
 
-def install(interp):
-    """Replace pmx.interp's parallel skeletons by the B200 versions.
-    Returns an `uninstall()` callable restoring the originals."""
+class DeviceList(list):
+    """A construct's result as the reference sees it (a Python list, fully
+    populated) that also carries its device sequence, so a later construct of
+    the same accelerate call consumes it without another upload."""
+
+    def __init__(self, values, dev=None):
+        super().__init__(values)
+        self.dev = dev
+
+
+class _WatchedBuffer(list):
+    """A heap buffer mirrored on the device: host-side writes (the
+    interpreter's tensorSet outside a construct, interp.py:471-474) mark the
+    device copy stale."""
+
+    def __init__(self, values, mirror):
+        super().__init__(values)
+        self.mirror = mirror
+
+    def __setitem__(self, k, v):
+        self.mirror.host_newer = True
+        list.__setitem__(self, k, v)
+
+
+class _Mirror:
+    """Device copy of one heap buffer for the duration of an accelerate call."""
+
+    def __init__(self, heap, bid):
+        from . import _lib
+        buf = heap.buffers[bid]
+        self.elem_float = bool(buf) and isinstance(buf[0], float)
+        if not isinstance(buf, _WatchedBuffer):
+            buf = _WatchedBuffer(buf, self)
+            heap.buffers[bid] = buf                 # the interpreter looks buffers up by id
+        self.buf = buf
+        self.data = None
+        self.host_newer = True
+        self.dtype_code = None
+        self.uploads = 0
+        self._lib = _lib
+
+    def device(self, elem: str):
+        import numpy as np
+        from .runtime import to_device
+        if self.data is None or self.host_newer:
+            np_t = np.float64 if elem == "float" else np.int64
+            self.data = to_device(np.array(self.buf, dtype=np_t))
+            self.dtype_code = self._lib.PMX_F64 if elem == "float" else self._lib.PMX_I64
+            self.host_newer = False
+            self.uploads += 1
+        return self.data
+
+    def copy_back(self):
+        vals = self.data.to("cpu").numpy().tolist()
+        if self.dtype_code == self._lib.PMX_F64:
+            vals = [float(v) for v in vals]
+        list.__setitem__(self.buf, slice(None), vals)   # coherent: not a host write
+
+
+class CallState:
+    """Device state of one accelerate call (`device_call` below): every host
+    sequence is uploaded at most once and construct results stay on the
+    device for the constructs that follow; every heap buffer a construct
+    touches is mirrored once and copied back after a construct writes it.
+    This is the single Alg. 2 marshal per accelerate (pmx/runtime.py:227-282)
+    on the device side: the reference's own marshal_in builds the roots, the
+    roots and sequences cross to the B200 once."""
+
+    def __init__(self, heap):
+        self.heap = heap
+        self.seqs: dict = {}
+        self.mirrors: dict = {}
+        self.h2d_sequences = 0
+
+    def seq(self, s):
+        from .runtime import seq_to_device
+        if isinstance(s, DeviceList) and s.dev is not None:
+            return s.dev
+        hit = self.seqs.get(id(s))
+        if hit is not None and hit[0] is s:
+            return hit[1]
+        d = seq_to_device(s)
+        self.seqs[id(s)] = (s, d)                   # keeps s alive: its id stays unique
+        self.h2d_sequences += 1
+        return d
+
+    def mirror(self, bid) -> _Mirror:
+        m = self.mirrors.get(bid)
+        if m is None:
+            m = self.mirrors[bid] = _Mirror(self.heap, bid)
+        return m
+
+
+def install(interp, *, device_call: bool = True):
+    """Replace pmx.interp's parallel skeletons (and, by default, its
+    `device_call`) by the B200 versions.  Returns an `uninstall()` callable
+    restoring the originals."""
     from . import skeletons as K
     from .diagnostics import Diagnostics as B200Diagnostics
-    from .runtime import seq_to_device, seq_to_host
+    from .runtime import seq_to_host
     pkg = interp.__name__.rsplit(".", 1)[0]
     syn = __import__(pkg + ".syntax", fromlist=["x"])
     rt = __import__(pkg + ".runtime", fromlist=["x"])
-    orig = {n: getattr(interp, n) for n in ("eval_map", "eval_map2", "eval_reduce", "eval_loop")}
+    names = ["eval_map", "eval_map2", "eval_reduce", "eval_loop"] + (["device_call"] if device_call else [])
+    orig = {n: getattr(interp, n) for n in names}
 
-    def translate(f, n, ctx, span, written):
+    def state(ctx) -> CallState:
+        cs = getattr(ctx, "_b200_call", None)
+        return cs if cs is not None else CallState(ctx.heap)   # per construct outside our device_call
+
+    def translate(f, n, ctx, span, touched, cs):
         def host_array(v):
             if isinstance(v, rt.TensorView):
-                t = HeapTensor(v, ctx.heap.buffers[v.buffer])
-                written.append(t)
+                t = HeapTensor(v, cs.mirror(v.buffer))
+                touched.append(t)
                 return t
-            return seq_to_device(v)
+            return cs.seq(v)
         try:
-            return to_lam(f, n, syn, rt, host_array)
+            lam = to_lam(f, n, syn, rt, host_array)
         except (Unsupported, CompileError) as exc:
             raise rt.runtime_error(f"not supported on the B200 device: {exc}", span) from None
+        _mark_written(lam, touched)
+        return lam
 
     def to_ref(seq):
         vals = seq_to_host(seq).tolist()
         if seq.elem_tag == "char":
-            return [chr(v) for v in vals]
-        if seq.elem_tag == "bool":
-            return [bool(v) for v in vals]
-        return vals
+            vals = [chr(v) for v in vals]
+        elif seq.elem_tag == "bool":
+            vals = [bool(v) for v in vals]
+        return DeviceList(vals, seq)
 
-    def run(f, n, ctx, span, body):
-        written: list = []
-        lam = translate(f, n, ctx, span, written)
-        dctx = K.Ctx()
+    def on_device(ctx, span, touched, body):
+        dctx = K.Ctx(check_determinism=bool(getattr(ctx, "check_determinism", False)))
         dctx.device = True
         K._ctx_stack.append(dctx)
         try:
-            out = body(lam)
+            out = body()
             dctx.check_errors()
         except B200Diagnostics as d:               # device error -> the reference's Diagnostics
             raise rt.runtime_error(d.items[0].message, span) from None
         finally:
             K._ctx_stack.pop()
-        for t in written:                           # tensors written by the construct
-            t.copy_back()
+        for t in touched:                           # tensors the construct wrote (tensorSet)
+            if t.written:
+                t.mirror.copy_back()
         return out
 
+    def run(f, n, ctx, span, body):
+        cs = state(ctx)
+        touched: list = []
+        lam = translate(f, n, ctx, span, touched, cs)
+        return on_device(ctx, span, touched, lambda: body(lam, cs))
+
     def run_rows(f, s, ctx, span):
-        written: list = []
+        cs = state(ctx)
+        touched: list = []
 
         def host_array(v):
             if isinstance(v, rt.TensorView):
-                t = HeapTensor(v, ctx.heap.buffers[v.buffer])
-                written.append(t)
+                t = HeapTensor(v, cs.mirror(v.buffer))
+                touched.append(t)
                 return t
-            return seq_to_device(v)
+            return cs.seq(v)
         try:
             g, op, acc = to_row_fold(f, syn, rt, host_array)
         except (Unsupported, CompileError) as exc:
             raise rt.runtime_error(f"not supported on the B200 device: {exc}", span) from None
-        dctx = K.Ctx()
-        dctx.device = True
-        K._ctx_stack.append(dctx)
-        try:
-            out = to_ref(K.map_rows_fold(g, op, acc, seq_to_device(s)))
-            dctx.check_errors()
-        except B200Diagnostics as d:
-            raise rt.runtime_error(d.items[0].message, span) from None
-        finally:
-            K._ctx_stack.pop()
-        return out
+        return on_device(ctx, span, touched, lambda: to_ref(K.map_rows_fold(g, op, acc, cs.seq(s))))
 
     def eval_map(f, s, ctx, span):
         if not ctx.run_parallel or not s:
@@ -541,25 +638,43 @@ def install(interp):
         if isinstance(s[0], list):                  # row function over [[a]]
             return run_rows(f, s, ctx, span)
         _elem_type(s)
-        return run(f, 1, ctx, span, lambda lam: to_ref(K._materialize(K.eval_map(lam, seq_to_device(s)))))
+        return run(f, 1, ctx, span, lambda lam, cs: to_ref(K._materialize(K.eval_map(lam, cs.seq(s)))))
 
     def eval_map2(f, s1, s2, ctx, span):
         if not ctx.run_parallel or not s1:
             return orig["eval_map2"](f, s1, s2, ctx, span)
-        return run(f, 2, ctx, span, lambda lam: to_ref(K.eval_map2(lam, s1, s2)))
+        return run(f, 2, ctx, span, lambda lam, cs: to_ref(K.eval_map2(lam, cs.seq(s1), cs.seq(s2))))
 
     def eval_reduce(f, acc, s, ctx, span):
         if not ctx.run_parallel or not s:
             return orig["eval_reduce"](f, acc, s, ctx, span)
-        return run(f, 2, ctx, span, lambda lam: K.eval_reduce(lam, acc, s).get())
+        return run(f, 2, ctx, span, lambda lam, cs: K.eval_reduce(lam, acc, cs.seq(s)).get())
 
     def eval_loop(n, f, ctx, span):
         if not ctx.run_parallel or n <= 0:
             return orig["eval_loop"](n, f, ctx, span)
-        return run(f, 1, ctx, span, lambda lam: K.eval_loop(n, lam))
+        return run(f, 1, ctx, span, lambda lam, cs: K.eval_loop(n, lam))
+
+    def b200_device_call(fn, args, ctx, span):
+        """interp.device_call (pmx/interp.py:230-237) with the device state of
+        the call: the reference's checks and Alg. 2 marshal_in, the body in
+        device context (its constructs run on the B200 and share one
+        CallState), then marshal_out."""
+        if ctx.checks:
+            for a in args:
+                interp._check_arg(fn.verdict, a, ctx)
+        dev_args, arena = interp.marshal_in(args, ctx.heap)
+        env = interp.Env(fn.env, dict(zip(fn.params, dev_args)))
+        dctx = ctx.device_clone()
+        dctx._b200_call = CallState(ctx.heap)
+        result = interp.eval_expr(fn.body, env, dctx)
+        install.last_call = dctx._b200_call
+        return interp.marshal_out(arena, ctx.heap, result)
 
     interp.eval_map, interp.eval_map2 = eval_map, eval_map2
     interp.eval_reduce, interp.eval_loop = eval_reduce, eval_loop
+    if device_call:
+        interp.device_call = b200_device_call
 
     def uninstall():
         for name, fn in orig.items():
@@ -567,39 +682,54 @@ def install(interp):
     return uninstall
 
 
+install.last_call = None
+
+
+def _mark_written(lam, touched):
+    """Flag the HeapTensors a lambda writes (TSet targets)."""
+    written = set()
+
+    def walk(e):
+        if isinstance(e, L.TSet):
+            written.add(id(e.tensor))
+        for v in getattr(e, "__dict__", {}).values():
+            if isinstance(v, L.Expr):
+                walk(v)
+            elif isinstance(v, (list, tuple)):
+                for x in v:
+                    if isinstance(x, L.Expr):
+                        walk(x)
+    walk(lam.body)
+    for t in touched:
+        t.written = t.written or id(t) in written
+
+
 class HeapTensor:
     """A reference TensorView (a view into a heap buffer, a Python list) used
-    by a device construct: the buffer is copied to the device on first use and
-    copied back after the construct (tensorSet effects, interp.py:471-474)."""
+    by a device construct, backed by the call's device mirror of that buffer
+    (uploaded once per accelerate call, copied back after a construct writes
+    it: the tensorSet effects of interp.py:471-474)."""
 
-    def __init__(self, view, heap_buf: list):
+    def __init__(self, view, mirror: _Mirror):
         from . import _lib
         self.view = view
-        self.heap_buf = heap_buf
+        self.mirror = mirror
         self.shape = tuple(view.shape)
         self.dtype_code = _lib.PMX_F64 if view.elem == "float" else _lib.PMX_I64
-        self.data = None
+        self.written = False
+
+    @property
+    def data(self):
+        return self.mirror.data
 
     def as_pmx_array(self):
-        import numpy as np
         from . import _lib
-        from .runtime import to_device
-        if self.data is None:
-            np_t = np.float64 if self.dtype_code == _lib.PMX_F64 else np.int64
-            self.data = to_device(np.array(self.heap_buf, dtype=np_t))
+        d = self.mirror.device(self.view.elem)
         a = _lib.Array()
-        a.data = self.data.data_ptr()
+        a.data = d.data_ptr()
         a.offset = self.view.offset
-        for i, d in enumerate(self.shape):
-            a.shape[i] = d
+        for i, n in enumerate(self.shape):
+            a.shape[i] = n
         a.rank = len(self.shape)
         a.dtype = self.dtype_code
         return a
-
-    def copy_back(self):
-        if self.data is None:
-            return
-        vals = self.data.to("cpu").numpy().tolist()
-        if self.view.elem == "float":
-            vals = [float(v) for v in vals]
-        self.heap_buf[:] = vals

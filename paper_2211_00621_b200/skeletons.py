@@ -366,7 +366,36 @@ def eval_reduce(f, acc, s, ctx: Optional[Ctx] = None, span: Span = NO_SPAN, *, k
     ctx.launches += 1
     if y is not None:
         s._value = DeviceSeq(y, src.shape, s.out_code, offsets=src.offsets, elem_tag=elem_t)
-    return DeviceScalar(out, acc_t == "float", err, span)
+    res = DeviceScalar(out, acc_t == "float", err, span)
+    if ctx.check_determinism:
+        _check_determinism(op, acc, acc_t, code, _materialize(s), res, ctx, span)
+    return res
+
+
+def _check_determinism(op, acc, acc_t, code, src, res, ctx, span):
+    """--check-determinism (pmx/interp.py:337-342, pmx/cli.py:41-42): re-fold
+    the sequence in element order on the device (one thread, pmx_fold without
+    a workspace) and warn, with the reference's message, when the tree
+    result differs beyond rel 1e-6 (interp.py:361-372)."""
+    import math
+    import sys
+    ref = torch.empty(1, dtype=torch.float64 if code == _lib.PMX_F64 else torch.int64, device=_device())
+    err = ctx.new_err(span)
+    init = _scalar_bits(acc, acc_t)
+    rc = _lib.load().pmx_fold(C.byref(op.program), src.ptr(), src.dtype_code, src.numel, C.byref(init), code,
+                              ref.data_ptr(), None, 0, err.data_ptr(), ctx.stream_ptr())
+    _lib.check(rc, "check_determinism fold")
+    ctx.launches += 1
+    total = res.get()
+    reference = DeviceScalar(ref, acc_t == "float", err, span).get()
+    if acc_t == "float":
+        close = math.isclose(total, reference, rel_tol=1e-6, abs_tol=1e-6)
+    else:
+        close = total == reference
+    if not close:
+        print("warning: reduce result depends on the evaluation order "
+              f"(blocked {total!r} vs sequential {reference!r}); the "
+              "operator may not be associative", file=sys.stderr)
 
 
 class PreparedMapReduce:

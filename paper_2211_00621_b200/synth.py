@@ -48,10 +48,11 @@ def mapreduce_exact_sum(n: int, a: float = 2.0, b: float = 1.0) -> float:
 
 
 # -------------------------------------------------------------------- RK4
-def rk4_params(n: int) -> np.ndarray:
-    """p_k = 0.5 + k/N (non-chaotic range)."""
-    k = np.arange(n, dtype=np.float64)
-    return 0.5 + k / float(n)
+def rk4_params(n: int, first: int = 0, total: int | None = None) -> np.ndarray:
+    """p_k = 0.5 + k/N (non-chaotic range); rows
+    [first, first + n) of an N = `total` (default n) parameter sweep."""
+    k = np.arange(first, first + n, dtype=np.float64)
+    return 0.5 + k / float(n if total is None else total)
 
 
 RK4_INIT = np.array([0.1, 0.0, 0.3, 0.0], dtype=np.float64)   # programs/rk4.pmx:41
@@ -65,8 +66,9 @@ def knn_train(ntr: int, d: int) -> np.ndarray:
     return ((_h(a, GOLD, 16) % 17) - 8).astype(np.float32).reshape(ntr, d)
 
 
-def knn_query(nq: int, d: int) -> np.ndarray:
-    a = np.arange(nq * d, dtype=np.int64)
+def knn_query(nq: int, d: int, first: int = 0) -> np.ndarray:
+    """queries [first, first + nq) of the query formula."""
+    a = np.arange(first * d, (first + nq) * d, dtype=np.int64)
     return ((_h(a, GOLD2, 16) % 17) - 8).astype(np.float32).reshape(nq, d)
 
 
@@ -95,9 +97,9 @@ def hmm_model(S: int, K: int):
     return A, E, pi
 
 
-def hmm_obs(nsig: int, T: int, K: int) -> np.ndarray:
-    """obs[s][t] = h(s*T + t) mod K."""
-    a = np.arange(nsig * T, dtype=np.int64)
+def hmm_obs(nsig: int, T: int, K: int, first: int = 0) -> np.ndarray:
+    """obs[s][t] = h(s*T + t) mod K, for signals [first, first + nsig)."""
+    a = np.arange(first * T, (first + nsig) * T, dtype=np.int64)
     return (_h(a, GOLD, 16) % K).astype(np.int32).reshape(nsig, T)
 
 

@@ -245,7 +245,8 @@ def main() -> None:
     g["alias"]["program"] = ALIAS_PROGRAM
 
     for prog in ("rk4", "viterbi", "nn"):
-        g[f"program_{prog}"] = run((REF / "programs" / f"{prog}.pmx").read_text(), mode="accel", workers=4)
+        src = (REF / "programs" / f"{prog}.pmx").read_text()
+        g[f"program_{prog}"] = dict(run(src, mode="accel", workers=4), program=src)
 
     g["rk4_param"] = []
     for n, m in ((6, 60), (3, 200)):

@@ -131,3 +131,68 @@ def test_hmm_forward_sparse_initial_distribution():
     want = O.hmm_forward_scaled(A, E, pi, obs)
     rel = np.abs(got - want) / np.abs(want)
     assert rel.max() <= LL_REL, float(rel.max())
+
+
+def test_viterbi_pruned_scan_with_nan_log_transitions():
+    # NaN entries of log A (possible through the C ABI, which takes log A
+    # directly) sort after every number in the pruned kernel's column order, so
+    # they neither win nor stop a scan early: same path as a dense max-plus that
+    # skips NaN candidates (first index on ties)
+    import torch
+    from paper_2211_00621_b200 import _lib
+    S, K, nsig, T = 256, 8, 3, 25
+    A, E, pi = synth.hmm_model(S, K)
+    lA = np.log(A)
+    rng = np.random.default_rng(5)
+    lA[rng.integers(0, S, 400), rng.integers(0, S, 400)] = np.nan
+    lE, lpi = np.log(E), np.log(pi)
+    obs = synth.hmm_obs(nsig, T, K)
+    want_path = np.empty((nsig, T), np.int32)
+    for s in range(nsig):
+        chi = lpi + lE[:, obs[s, 0]]
+        back = []
+        for t in range(1, T):
+            cand = chi[:, None] + lA
+            arg = np.nanargmax(cand, axis=0)
+            back.append(arg)
+            chi = cand[arg, np.arange(S)] + lE[:, obs[s, t]]
+        st = int(np.argmax(chi))
+        want_path[s, T - 1] = st
+        for t in range(T - 1, 0, -1):
+            st = int(back[t - 1][st])
+            want_path[s, t - 1] = st
+    dev = torch.device("cuda")
+    t_lA, t_lE, t_lpi = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (lA, lE, lpi))
+    t_obs = torch.from_numpy(obs).to(dev)
+    path = torch.empty(nsig * T, dtype=torch.int32, device=dev)
+    logp = torch.empty(nsig, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    ws = torch.empty(lib.pmx_viterbi_workspace_bytes(S, nsig, T), dtype=torch.uint8, device=dev)
+    st_ = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.pmx_viterbi_f64(t_lpi.data_ptr(), t_lA.data_ptr(), t_lE.data_ptr(), S, K, t_obs.data_ptr(), nsig,
+                                   T, path.data_ptr(), logp.data_ptr(), ws.data_ptr(), ws.numel(), st_), "viterbi")
+    assert lib.pmx_viterbi_visited_cells(ws.data_ptr(), S, nsig, T, st_) > 0
+    assert np.array_equal(path.cpu().numpy().reshape(nsig, T), want_path)
+
+
+def test_viterbi_visited_cells_counter():
+    # the pruned kernel's work counter (the Viterbi roofline's numerator): at most
+    # the dense cell count, and a small fraction of it on the bench model
+    import torch
+    from paper_2211_00621_b200 import _lib
+    S, K, nsig, T = 1024, 8, 16, 50
+    A, E, pi = synth.hmm_model(S, K)
+    dev = torch.device("cuda")
+    lA, lE, lpi = (torch.from_numpy(np.log(a)).to(dev) for a in (A, E, pi))
+    obs = torch.from_numpy(synth.hmm_obs(nsig, T, K)).to(dev)
+    path = torch.empty(nsig * T, dtype=torch.int32, device=dev)
+    logp = torch.empty(nsig, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    ws = torch.empty(lib.pmx_viterbi_workspace_bytes(S, nsig, T), dtype=torch.uint8, device=dev)
+    st_ = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.pmx_viterbi_f64(lpi.data_ptr(), lA.data_ptr(), lE.data_ptr(), S, K, obs.data_ptr(), nsig, T,
+                                   path.data_ptr(), logp.data_ptr(), ws.data_ptr(), ws.numel(), st_), "viterbi")
+    v = lib.pmx_viterbi_visited_cells(ws.data_ptr(), S, nsig, T, st_)
+    dense = S * S * (T - 1) * 16          # 8-signal CTAs: 2 CTAs, padding-free here
+    assert 0 < v <= dense
+    assert v < 0.5 * dense, v / dense

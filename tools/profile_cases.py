@@ -111,6 +111,45 @@ def kmer(reps=2, T=100):
     torch.cuda.synchronize()
 
 
+def viterbi(reps=2, T=100):
+    S, K, nsig = 1024, 8, 148 * 8
+    A, E, pi = synth.hmm_model(S, K)
+    lA, lE, lpi = (torch.from_numpy(np.log(a)).cuda() for a in (A, E, pi))
+    obs = torch.from_numpy(synth.hmm_obs(nsig, T, K)).cuda()
+    path = torch.empty(nsig * T, dtype=torch.int32, device="cuda")
+    logp = torch.empty(nsig, dtype=torch.float64, device="cuda")
+    lib = _lib.load()
+    ws = torch.empty(lib.pmx_viterbi_workspace_bytes(S, nsig, T), dtype=torch.uint8, device="cuda")
+    for _ in range(reps):
+        _lib.check(lib.pmx_viterbi_f64(lpi.data_ptr(), lA.data_ptr(), lE.data_ptr(), S, K, obs.data_ptr(), nsig, T,
+                                       path.data_ptr(), logp.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       torch.cuda.current_stream().cuda_stream), "viterbi")
+    torch.cuda.synchronize()
+    v = lib.pmx_viterbi_visited_cells(ws.data_ptr(), S, nsig, T, torch.cuda.current_stream().cuda_stream)
+    print("viterbi visited cells per launch", v, "of", S * S * (T - 1) * nsig)
+
+
+def nn(reps=2):
+    npts, nin, nout = 1 << 20, 64, 16
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(npts * nin, dtype=torch.float64, device="cuda", generator=g) * 0.5
+    y = torch.randint(0, nout, (npts,), dtype=torch.int32, device="cuda", generator=g)
+    w = torch.randn(nin * nout, dtype=torch.float64, device="cuda", generator=g) * 0.3
+    b = torch.randn(nout, dtype=torch.float64, device="cuda", generator=g) * 0.1
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    dw = torch.empty(nin * nout, dtype=torch.float64, device="cuda")
+    db = torch.empty(nout, dtype=torch.float64, device="cuda")
+    err = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    lib = _lib.load()
+    ws = torch.zeros(lib.pmx_nn_workspace_bytes(npts, nin, nout), dtype=torch.uint8, device="cuda")
+    for _ in range(reps):
+        _lib.check(lib.pmx_nn_softmax_grad_f64(x.data_ptr(), y.data_ptr(), w.data_ptr(), b.data_ptr(), npts, nin,
+                                               nout, loss.data_ptr(), dw.data_ptr(), db.data_ptr(), ws.data_ptr(),
+                                               ws.numel(), err.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                   "nn")
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
     P.load_library()
     for name in sys.argv[1:] or ["mapreduce"]:

@@ -1,8 +1,10 @@
 """Runtime assumption checks (§5.1 of the paper), run on the host before
 marshalling when `Ctx(checks=True)` — mirrors pmx/runtime.py:115-138 and
 pmx/interp.py:223-227 (`_check_arg`).  The reference picks the check by the
-binding's backend verdict; without the compiler here both are applied: nested
-sequences must be regular, tensors must have rank <= max_rank."""
+binding's backend verdict (Classification.FUTHARK -> regular sequences,
+Classification.CUDA -> tensor rank <= max_rank); `check_arg` does the same when
+given a verdict ("futhark" / "cuda", or the reference's enum member) and
+applies both when the verdict is unknown (None)."""
 from __future__ import annotations
 
 import numpy as np
@@ -36,6 +38,17 @@ def check_ranks(value, max_rank: int) -> None:
         check_rank(t, max_rank)
 
 
-def check_arg(value, max_rank: int) -> None:
-    check_regular(value)
-    check_ranks(value, max_rank)
+def _verdict_name(verdict) -> str | None:
+    if verdict is None:
+        return None
+    name = getattr(verdict, "name", verdict)      # pmx.classify.Classification member or a string
+    return str(name).lower()
+
+
+def check_arg(value, max_rank: int, verdict=None) -> None:
+    """`_check_arg(verdict, value, ctx)` (pmx/interp.py:223-227)."""
+    v = _verdict_name(verdict)
+    if v in (None, "futhark"):
+        check_regular(value)
+    if v in (None, "cuda"):
+        check_ranks(value, max_rank)

@@ -618,18 +618,21 @@ def length(s) -> int:
 
 # ------------------------------------------------------------ accelerate
 
-def device_call(fn, args: list, ctx: Optional[Ctx] = None, span: Span = NO_SPAN):
+def device_call(fn, args: list, ctx: Optional[Ctx] = None, span: Span = NO_SPAN, verdict=None):
     """The accelerate entry point (pmx/interp.py:230-237): marshal the
     arguments to the device (Alg. 2), evaluate the body in a device context,
     check device errors, copy written roots back and return host values.
 
     `fn` is a Python callable over device values built from this module's
-    operators (the lifted accelerate binding, pmx/transform.py:198-317)."""
+    operators (the lifted accelerate binding, pmx/transform.py:198-317).
+    `verdict` is the binding's backend classification ("futhark" / "cuda");
+    it selects which assumption check `ctx.checks` runs (pmx/interp.py:223-227),
+    both when None."""
     ctx = ctx or Ctx()
     if ctx.checks:
         from .checks import check_arg
         for a in args:
-            check_arg(a, ctx.max_rank)
+            check_arg(a, ctx.max_rank, verdict)
     dev_args, arena = marshal_in(list(args), ctx.heap)
     dctx = ctx.device_clone()
     _ctx_stack.append(dctx)
@@ -666,6 +669,6 @@ def _takes_ctx(fn) -> bool:
         return False
 
 
-def accelerate(fn, *args, ctx: Optional[Ctx] = None, span: Span = NO_SPAN):
+def accelerate(fn, *args, ctx: Optional[Ctx] = None, span: Span = NO_SPAN, verdict=None):
     """`accelerate (fn args...)` — run fn on the B200 with its arguments marshalled."""
-    return device_call(fn, list(args), ctx, span)
+    return device_call(fn, list(args), ctx, span, verdict)

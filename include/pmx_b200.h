@@ -221,6 +221,11 @@ PMX_API int pmx_seq_loop(const pmx_program* f, double* state, double* scratch,
 PMX_API int pmx_scan_lengths(const int64_t* lengths, int64_t* offsets, int64_t n,
                      void* stream);
 
+/* offsets[i] = i * row_len for i in [0, nrows]: the row offsets of a regular
+ * nested sequence, so row kernels take one layout for regular and irregular
+ * rows.                              used by the row-fold map (interp.py:294-304) */
+PMX_API int pmx_row_offsets(int64_t* offsets, int64_t nrows, int64_t row_len, void* stream);
+
 /* ---- run-time kernel specialisation ---------------------------------------
  * A lambda the library does not recognise runs, above a size threshold, in
  * the streaming skeleton kernel specialised to it: its bytecode is translated

@@ -104,6 +104,7 @@ _SIGS = {
                                     C.c_int32, _P, _P]),
     "pmx_seq_loop": (C.c_int, [C.POINTER(Program), _P, _P, C.c_int64, C.c_int64, _P, _P]),
     "pmx_scan_lengths": (C.c_int, [_P, _P, C.c_int64, _P]),
+    "pmx_row_offsets": (C.c_int, [_P, C.c_int64, C.c_int64, _P]),
     "pmx_rk4_sweep_f64": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_double, _P, _P]),
     "pmx_rk4_trace_f64": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_double, C.c_int32, _P, _P, _P]),
     "pmx_hmm_forward_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int64]),

@@ -372,6 +372,12 @@ __global__ void k_copy_f64(const double* s, double* d, int64_t m) {
         d[j] = s[j];
 }
 
+// offsets of a regular nested sequence: off[i] = i * row_len, i in [0, nrows]
+__global__ void k_row_offsets(int64_t* off, int64_t nrows, int64_t row_len) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nrows; i += (int64_t)gridDim.x * blockDim.x)
+        off[i] = i * row_len;
+}
+
 // Exclusive scan of lengths into n+1 offsets with one CTA: each thread scans
 // a contiguous chunk, block scan of chunk totals, then write.
 __global__ void k_scan_lengths(const int64_t* len, int64_t* off, int64_t n) {
@@ -727,6 +733,14 @@ int pmx_seq_loop(const pmx_program* f, double* state, double* scratch, int64_t m
         k_copy_f64<<<grid_for(m, 256, 4), 256, 0, st>>>(scratch, state, m);
         PMX_CHECK_LAUNCH("seq_loop copy");
     }
+    return 0;
+}
+
+int pmx_row_offsets(int64_t* offsets, int64_t nrows, int64_t row_len, void* stream) {
+    PMX_REQUIRE(offsets, "pmx_row_offsets: null offsets");
+    PMX_REQUIRE(nrows >= 0 && row_len >= 0, "pmx_row_offsets: negative size");
+    k_row_offsets<<<grid_for(nrows + 1, 256, 4), 256, 0, (cudaStream_t)stream>>>(offsets, nrows, row_len);
+    PMX_CHECK_LAUNCH("row_offsets");
     return 0;
 }
 

@@ -323,6 +323,7 @@ class _Gen:
         self.consts: list[int] = []
         self.const_ix: dict[tuple, int] = {}
         self.arrays: list[Any] = []
+        self.written: set[int] = set()          # arrays a TSET stores into
         self.free = list(range(_lib.MAX_REGS - 1, n_inputs - 1, -1))  # pop() gives lowest
         self.n_inputs = n_inputs
 
@@ -498,6 +499,7 @@ def _compile(e: Expr, env: dict, g: _Gen) -> tuple[int, str, bool]:
             return dst, DTYPE_TYPE[t.dtype_code], True
         v, vt, vown = _compile(e.value, env, g)
         g.emit("TSET", 0, base, v, k)
+        g.written.add(k)
         if vown:
             g.release(v)
         for d in range(len(e.index)):
@@ -615,5 +617,5 @@ def _lower(fl: Lam, in_types: list[str], state_array) -> Compiled:
     for i, v in enumerate(g.consts):
         prog.consts[i] = v
     for i, arr in enumerate(g.arrays):
-        prog.arrays[i] = arr.as_pmx_array()
+        prog.arrays[i] = arr.as_pmx_array(write=i in g.written)
     return Compiled(prog, t, insns=[list(x) for x in g.insns])

@@ -732,7 +732,7 @@ class HeapTensor:
     def data(self):
         return self.mirror.data
 
-    def as_pmx_array(self):
+    def as_pmx_array(self, write: bool = True):
         from . import _lib
         d = self.mirror.device(self.view.elem)
         a = _lib.Array()

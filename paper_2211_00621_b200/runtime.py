@@ -174,7 +174,7 @@ class DeviceSeq(DeviceValue):
     def numel(self) -> int:
         return self.data.numel()
 
-    def as_pmx_array(self) -> _lib.Array:
+    def as_pmx_array(self, write: bool = True) -> _lib.Array:
         a = _lib.Array()
         a.data = self.data.data_ptr()
         a.offset = 0
@@ -222,7 +222,7 @@ class DeviceTensor(DeviceValue):
     def size(self) -> int:
         return math.prod(self.shape)
 
-    def as_pmx_array(self) -> _lib.Array:
+    def as_pmx_array(self, write: bool = True) -> _lib.Array:
         if len(self.shape) > _lib.MAX_RANK:
             raise runtime_error(f"tensor rank {len(self.shape)} exceeds the device bound {_lib.MAX_RANK}")
         a = _lib.Array()
@@ -232,7 +232,8 @@ class DeviceTensor(DeviceValue):
             a.shape[i] = d
         a.rank = len(self.shape)
         a.dtype = self.root.dtype_code
-        self.root.dirty = True      # conservatively: any kernel holding the view may write it
+        if write:                   # only a root some kernel stores into is copied back
+            self.root.dirty = True
         return a
 
 
@@ -299,6 +300,17 @@ def to_device(arr, arena: Optional[DeviceArena] = None):
     return dev
 
 
+def lengths_to_offsets(lens, arena: Optional[DeviceArena] = None):
+    """Row offsets of an irregular sequence, built on the device: the row
+    lengths are copied up and pmx_scan_lengths writes the n+1 offsets
+    (flatten is then the values buffer itself, pmx/interp.py:161-166)."""
+    d_lens = to_device(np.asarray(lens, np.int64), arena)
+    offs = torch.empty(len(lens) + 1, dtype=torch.int64, device=_device())
+    _lib.check(_lib.load().pmx_scan_lengths(d_lens.data_ptr(), offs.data_ptr(), len(lens),
+                                            torch.cuda.current_stream().cuda_stream), "scan lengths")
+    return offs
+
+
 def _is_char_list(v) -> bool:
     return isinstance(v, list) and v and all(isinstance(c, str) and len(c) == 1 for c in v)
 
@@ -331,9 +343,7 @@ def seq_to_device(v, arena: Optional[DeviceArena] = None) -> DeviceValue:
             return inner
         flat = [x for r in v for x in r]
         inner = seq_to_device(flat, arena) if flat else DeviceSeq(to_device(np.zeros(0, np.int64), arena), (0,), _lib.PMX_I64)
-        offs = np.zeros(len(v) + 1, np.int64)
-        offs[1:] = np.cumsum(lens)
-        return DeviceSeq(inner.data, (len(v),), inner.dtype_code, offsets=to_device(offs, arena),
+        return DeviceSeq(inner.data, (len(v),), inner.dtype_code, offsets=lengths_to_offsets(lens, arena),
                          elem_tag=inner.elem_tag)
     if isinstance(x0, bool):
         return DeviceSeq(to_device(np.array(v, np.uint8), arena), (len(v),), _lib.PMX_BOOL)

@@ -243,8 +243,8 @@ class LazyMap(DeviceValue):
     def ptr(self):
         return self.materialize().ptr()
 
-    def as_pmx_array(self):
-        return self.materialize().as_pmx_array()
+    def as_pmx_array(self, write: bool = True):
+        return self.materialize().as_pmx_array(write)
 
 
 def _materialize(s):
@@ -521,7 +521,9 @@ def map_rows_fold(g, op, acc, s, ctx: Optional[Ctx] = None, span: Span = NO_SPAN
         nrows, offs = len(s), s.offsets
     elif s.rank == 2:
         nrows, m = s.shape
-        offs = torch.arange(nrows + 1, dtype=torch.int64, device=_device()) * m
+        offs = torch.empty(nrows + 1, dtype=torch.int64, device=_device())
+        _lib.check(_lib.load().pmx_row_offsets(offs.data_ptr(), nrows, m, ctx.stream_ptr()), "row offsets")
+        ctx.launches += 1
     else:
         raise runtime_error("a row function needs a sequence of sequences", span)
     if isinstance(acc, DeviceScalar):
@@ -573,7 +575,8 @@ def seq_loop(n: int, f, state, ctx: Optional[Ctx] = None, span: Span = NO_SPAN) 
     the captured placeholder `PREV` (see lam.get)."""
     ctx = ctx or default_ctx()
     s = _materialize(_as_seq(state, "seqLoop", span))
-    a = s.data.to(torch.float64).clone()
+    from .lambdas import lam
+    a = map_tensor(lam("x", "x"), s.data, _lib.PMX_F64, span)        # fresh fp64 state (one pmx_map)
     b = torch.empty(a.numel() + 8, dtype=torch.float64, device=a.device)   # + grid-barrier word
     prog = _compile(f, ["float", "int", "int"], span, state_array=PREV)
     err = ctx.new_err(span)
@@ -588,7 +591,7 @@ class _PrevState:
     """Placeholder for the previous seqLoop state inside a step lambda."""
     dtype_code = _lib.PMX_F64
 
-    def as_pmx_array(self):
+    def as_pmx_array(self, write: bool = True):
         a = _lib.Array()
         a.rank = 1
         a.dtype = _lib.PMX_F64

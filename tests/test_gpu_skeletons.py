@@ -150,6 +150,24 @@ def test_tensor_sub_alias(golden):
     assert int(r[0]) == int(out[0]) and int(heap.buffers[b][5]) == int(out[1])
 
 
+def test_read_only_view_not_copied_back():
+    # a root that no kernel stores into (only tensor_get) is not copied back
+    # by marshal_out; a written one is (pmx/runtime.py:262-282)
+    heap = Heap()
+    b = heap.alloc(np.arange(16, dtype=np.int64))
+    t = TensorView(b, 0, (16,), "int")
+    ctx = Ctx(heap=heap)
+    r = accelerate(lambda tt: eval_reduce(addi, 0, eval_map(lam("i", tensor_get(tt, ["i"])), list(range(16)))),
+                   t, ctx=ctx)
+    assert r == sum(range(16))
+    assert not any(root.dirty for root in ctx.last_arena.roots)
+    assert ctx.last_arena.d2h_bytes <= 8                  # the scalar result only
+    ctx = Ctx(heap=heap)
+    accelerate(lambda tt: eval_loop(16, lam("i", tensor_set(tt, ["i"], muli("i", 2)))), t, ctx=ctx)
+    assert all(root.dirty for root in ctx.last_arena.roots)
+    assert int(heap.buffers[b][15]) == 30
+
+
 def test_tensor_oob_is_an_error():
     heap = Heap()
     b = heap.alloc(np.zeros(2, np.int64))

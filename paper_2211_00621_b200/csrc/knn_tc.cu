@@ -17,7 +17,7 @@
 // 16-wide augmentation (A rows [256, 1, 0...], B rows [hi, lo, 0...],
 // SWIZZLE_32B).  The epilogue is then one min per candidate.
 //
-// Structure (persistent, one CTA per SM, 12 warps):
+// Structure (persistent, one CTA per SM, 20 warps):
 //   warp 0   TMA producer: the 256-query block A (2 x 128 rows) once per work
 //            item; train tiles B (128 x 64 bf16 of -2x) + B_aug (128 x 16)
 //            through a 4-stage ring
@@ -25,14 +25,21 @@
 //            accumulators (one per 128-query half) into one of two TMEM
 //            buffers (2 buffers x 2 halves x 128 columns = all 512 columns)
 //   warp 2   TMEM allocator
-//   warps 4-11 epilogue: warp w owns query half (w-4)/4 and TMEM lane
-//            quadrant w%4 (one query per thread) and scans the tile's 128
-//            candidates: 2 x (64-column tcgen05.ld), min-tree per 32, and the
-//            rare sorted insertion of (order-preserving distance bits, index)
+//   warps 4-19 epilogue: warp w owns TMEM lane quadrant w%4 (one query per
+//            thread), query half ((w-4)>>2)&1 and column half (w-4)>>3, and
+//            scans its 64 candidates of the tile in two 32-column loads: a
+//            min-tree per 8, a warp vote, and the rare branch-free insertion
+//            into a register-resident sorted top-8 (distance, index)
 // Work item = (256-query block, contiguous range of train tiles).  Reusing
-// each B tile for 256 queries halves L2 traffic versus 128; splitting the
-// train range balances the blocks over 148 SMs.  Per-item partial top-k lists
-// go to global memory; k_knn_merge merges them and votes.
+// each B tile for 256 queries halves L2 traffic versus 128; the split count
+// is chosen so the items fill whole rounds of the SMs (all SMs with the same
+// split stream the same train tiles in lockstep, so B tiles hit in L2).
+// Per-item partial top-8 lists (two per query: one per column half) go to
+// global memory; k_knn_merge merges them and votes.
+//
+// Measured bound (tools/tmem_probe.cu, profiles/tmem_probe.json): TMEM reads
+// run at ~178 B/clk/SM, so a tile's 128 KiB of candidates needs ~740 clk
+// against ~640 clk of UMMA (M = 128, N = 128, K = 80, two halves).
 #include <cuda_bf16.h>
 #include "common.cuh"
 #include "tc.cuh"
@@ -46,7 +53,9 @@ constexpr int KT_D = 64;
 constexpr int KT_AUG = 16;
 constexpr int KT_STAGES = 4;
 constexpr int KT_KMAX = 8;
-constexpr int KT_THREADS = 384;
+constexpr int KT_EW = 16;                 // epilogue warps
+constexpr int KT_THREADS = 128 + 32 * KT_EW;
+constexpr int KT_LPQ = 2;                 // partial lists per query per item (column halves)
 constexpr uint32_t KT_A_BYTES = KT_Q * KT_D * 2;        // 32 KB
 constexpr uint32_t KT_B_BYTES = KT_N * KT_D * 2;        // 16 KB
 constexpr uint32_t KT_BAUG_BYTES = KT_N * KT_AUG * 2;   //  4 KB
@@ -70,17 +79,58 @@ __device__ __forceinline__ float unord_f32(uint32_t u) {
     return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
 }
 
-// insert (dv, idx) into the sorted list; returns the new k-th threshold.
-// Entries arrive in increasing index order per list, so an equal distance
-// never displaces an existing entry: ties keep the smaller index.
-__device__ __noinline__ float knn_insert(uint64_t* L, int k, float dv, uint32_t idx) {
-    const uint64_t key = ((uint64_t)ord_f32(dv) << 32) | idx;
-    int p = k - 1;
-    if (L[p] > key) {
-        while (p > 0 && L[p - 1] > key) { L[p] = L[p - 1]; --p; }
-        L[p] = key;
+// Sorted top-8 of one thread, in registers: d ascending, ties by arrival
+// (candidates arrive in increasing train index, and an equal distance never
+// displaces an entry, so ties keep the smaller index).  Branch-free: every
+// slot is a select, so the compiler keeps d/x in registers (no local memory).
+struct Top8 {
+    float d[KT_KMAX];
+    uint32_t x[KT_KMAX];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int i = 0; i < KT_KMAX; ++i) { d[i] = __int_as_float(0x7f800000); x[i] = 0xffffffffu; }
     }
-    return L[k - 1] == ~0ull ? __int_as_float(0x7f800000) : unord_f32((uint32_t)(L[k - 1] >> 32));
+    // caller guarantees dv < d[KT_KMAX - 1] for a real insertion; otherwise a no-op
+    __device__ __forceinline__ void insert(float dv, uint32_t ix) {
+#pragma unroll
+        for (int i = KT_KMAX - 1; i > 0; --i) {
+            const bool shift = dv < d[i - 1];
+            const bool here = dv < d[i];
+            d[i] = shift ? d[i - 1] : (here ? dv : d[i]);
+            x[i] = shift ? x[i - 1] : (here ? ix : x[i]);
+        }
+        const bool first = dv < d[0];
+        d[0] = first ? dv : d[0];
+        x[0] = first ? ix : x[0];
+    }
+    __device__ __forceinline__ uint64_t key(int i) const {
+        return x[i] == 0xffffffffu ? ~0ull : (((uint64_t)ord_f32(d[i]) << 32) | x[i]);
+    }
+};
+
+// Scan 32 candidate distances (column base col0) into the list: a min over
+// each 8 (depth-3 trees), one vote per 8 against the threshold, and for a
+// group some lane needs, one vote per candidate gating the predicated insert.
+__device__ __forceinline__ void knn_scan32(const uint32_t (&r)[32], int64_t col0, Top8& L) {
+    float m8[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        float a[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[j] = fminf(__uint_as_float(r[g * 8 + j]), __uint_as_float(r[g * 8 + j + 4]));
+        m8[g] = fminf(fminf(a[0], a[1]), fminf(a[2], a[3]));
+    }
+    const float thr = L.d[KT_KMAX - 1];
+    if (!__any_sync(0xffffffffu, fminf(fminf(m8[0], m8[1]), fminf(m8[2], m8[3])) < thr)) return;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        if (!__any_sync(0xffffffffu, m8[g] < L.d[KT_KMAX - 1])) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float dv = __uint_as_float(r[g * 8 + j]);
+            if (__any_sync(0xffffffffu, dv < L.d[KT_KMAX - 1])) L.insert(dv, (uint32_t)(col0 + g * 8 + j));
+        }
+    }
 }
 
 // prep (d == 64), 16 lanes per row, one float4 per lane (coalesced):
@@ -153,7 +203,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         for (int s = 0; s < KT_STAGES; ++s) { tc::mbar_init(&S.full[s], 1); tc::mbar_init(&S.empty[s], 1); }
         tc::mbar_init(&S.a_full, 1);
         tc::mbar_init(&S.a_empty, 1);
-        for (int b = 0; b < 2; ++b) { tc::mbar_init(&S.tfull[b], 1); tc::mbar_init(&S.tempty[b], 8); }
+        for (int b = 0; b < 2; ++b) { tc::mbar_init(&S.tfull[b], 1); tc::mbar_init(&S.tempty[b], KT_EW); }
         tc::fence_mbar_init();
         tc::tma_prefetch(&tmq);
         tc::tma_prefetch(&tmx);
@@ -237,64 +287,46 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
             __syncwarp();
         }
     } else if (warp >= 4) {                                  // ---- epilogue
-        const int quad = warp & 3, h = (warp - 4) >> 2;
+        const int ew = warp - 4;
+        const int quad = warp & 3, h = (ew >> 2) & 1, ch = ew >> 3;
         const int row = h * KT_M + quad * 32 + lane;           // query within the block
         int b = 0; uint32_t acc_phase = 0;
-        uint64_t L[KT_KMAX];                                  // sorted keys (touched on insertion only)
+        Top8 L;
         for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
             const int qb = it / nsplit, sp = it % nsplit;
             const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
-            for (int i = 0; i < KT_KMAX; ++i) L[i] = ~0ull;
-            float thr = __int_as_float(0x7f800000);        // +inf
+            L.reset();
             for (int t = t0; t < t1; ++t) {
                 tc::mbar_wait(&S.tfull[b], acc_phase);
                 tc::tc_fence_after();
-                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((b * 2 + h) * KT_N);
-                const int64_t colbase = (int64_t)t * KT_N;
+                const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((b * 2 + h) * KT_N + ch * 64);
+                const int64_t colbase = (int64_t)t * KT_N + ch * 64;
 #pragma unroll 1
                 for (int c = 0; c < 2; ++c) {
-                    uint32_t r[64];
-                    tc::tmem_ld_32x32b_x64(taddr + c * 64, r);
+                    uint32_t r[32];
+                    tc::tmem_ld_32x32b_x32(taddr + c * 32, r);
                     tc::tmem_ld_wait();
-                    if (c == 1) {                             // accumulator fully read: release it
+                    if (c == 1) {                             // my columns fully read: release
                         tc::tc_fence_before();
                         __syncwarp();
                         if (lane == 0) tc::mbar_arrive(&S.tempty[b]);
                     }
-                    const int64_t col0 = colbase + c * 64;
-                    if (col0 + 64 > ntr) {                   // last tile: padded rows read as 0
+                    const int64_t col0 = colbase + c * 32;
+                    if (col0 + 32 > ntr) {                   // last tile: padded rows read as +inf
 #pragma unroll
-                        for (int j = 0; j < 64; ++j)
+                        for (int j = 0; j < 32; ++j)
                             if (col0 + j >= ntr) r[j] = 0x7f800000u;
                     }
-                    // per 32 candidates: min as a depth-5 tree (a linear chain
-                    // would serialise 31 dependent FMNMX), then the rare scan
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) {
-                        float m[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            m[j] = fminf(__uint_as_float(r[g * 32 + j]), __uint_as_float(r[g * 32 + j + 16]));
-#pragma unroll
-                        for (int w = 8; w > 0; w >>= 1)
-#pragma unroll
-                            for (int j = 0; j < w; ++j) m[j] = fminf(m[j], m[j + w]);
-                        if (m[0] < thr) {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                const float dv = __uint_as_float(r[g * 32 + j]);
-                                if (dv < thr) thr = knn_insert(L, k, dv, (uint32_t)(col0 + g * 32 + j));
-                            }
-                        }
-                    }
+                    knn_scan32(r, col0, L);
                 }
                 b ^= 1;
                 if (b == 0) acc_phase ^= 1;
             }
             const int64_t q = (int64_t)qb * KT_Q + row;
             if (q < nq) {
-                uint64_t* dst = lists + (q * nsplit + sp) * KT_KMAX;
-                for (int i = 0; i < KT_KMAX; ++i) dst[i] = L[i];
+                uint64_t* dst = lists + ((q * nsplit + sp) * KT_LPQ + ch) * KT_KMAX;
+#pragma unroll
+                for (int i = 0; i < KT_KMAX; ++i) dst[i] = L.key(i);
             }
         }
     }
@@ -366,13 +398,22 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int 
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Split count: items fill whole rounds of the SMs (rounds x tiles per item is
+// the kernel's length in tile times), with a 1% charge per split for the
+// per-item restart of the top-8 lists (early tiles insert often).
 int knn_tc_nsplit(int64_t ntr, int64_t nq) {
-    const int nblk = (int)((nq + KT_Q - 1) / KT_Q);
-    const int ntiles = (int)((ntr + KT_N - 1) / KT_N);
-    int ns = (4 * sm_count() + nblk - 1) / nblk;       // ~4 work items per SM
-    if (ns > 64) ns = 64;
-    if (ns > ntiles) ns = ntiles;
-    return ns < 1 ? 1 : ns;
+    const int64_t nblk = (nq + KT_Q - 1) / KT_Q;
+    const int64_t ntiles = (ntr + KT_N - 1) / KT_N;
+    const int64_t sms = sm_count();
+    int best = 1;
+    double best_cost = 1e300;
+    for (int ns = 1; ns <= 32 && ns <= ntiles; ++ns) {
+        const int64_t rounds = (nblk * ns + sms - 1) / sms;
+        const int64_t per = (ntiles + ns - 1) / ns;
+        const double cost = (double)(rounds * per) * (1.0 + 0.01 * ns);
+        if (cost < best_cost) { best_cost = cost; best = ns; }
+    }
+    return best;
 }
 
 // workspace: xb (ntr x 64 bf16) | xaug (ntr x 16 bf16) | qb (nq x 64 bf16) | lists
@@ -384,7 +425,7 @@ static inline int64_t pad_to(int64_t n, int64_t m) { return (n + m - 1) / m * m;
 size_t knn_tc_workspace(int64_t ntr, int64_t nq) {
     const int ns = knn_tc_nsplit(ntr, nq);
     const int64_t ntr_p = pad_to(ntr, KT_N), nq_p = pad_to(nq, KT_Q);
-    return (size_t)ntr_p * (KT_D + KT_AUG) * 2 + (size_t)nq_p * KT_D * 2 + 1024 + (size_t)nq * ns * KT_KMAX * 8 + 256;
+    return (size_t)ntr_p * (KT_D + KT_AUG) * 2 + (size_t)nq_p * KT_D * 2 + 1024 + (size_t)nq * ns * KT_LPQ * KT_KMAX * 8 + 256;
 }
 
 int knn_tc_run(const float* train, const float* query, const int* labels, int64_t ntr, int64_t nq, int k, int ncls,
@@ -416,7 +457,7 @@ int knn_tc_run(const float* train, const float* query, const int* labels, int64_
     const int grid = nitems < sm_count() ? nitems : sm_count();
     k_knn_tc<<<grid, KT_THREADS, smem, st>>>(tmq, tmx, tmxa, ntr, nq, k, nsplit, lists, flag);
     PMX_CHECK_LAUNCH("knn_tc");
-    k_knn_merge<<<(unsigned)((nq + 127) / 128), 128, 0, st>>>(lists, nsplit, labels, nq, k, ncls, out_label,
+    k_knn_merge<<<(unsigned)((nq + 127) / 128), 128, 0, st>>>(lists, nsplit * KT_LPQ, labels, nq, k, ncls, out_label,
                                                               out_idx, flag);
     PMX_CHECK_LAUNCH("knn_merge");
     return 0;

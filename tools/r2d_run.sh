@@ -1,0 +1,11 @@
+# r2d: k-NN epilogue v2 (16 epilogue warps, register top-8): parity tests + timing + ncu
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "knn" > gpurun_out/pytest_knn.log 2>&1
+tail -3 gpurun_out/pytest_knn.log
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu --case knn > gpurun_out/bench_knn.json 2> gpurun_out/bench_knn.err
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_knn.json').read().strip().splitlines()[-1]); k=d['case_studies']['knn']; print('knn ms', k.get('ms_per_step'), k.get('roofline',{}).get('frac'), k.get('parity'))"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_knn_tc -c 1 -o gpurun_out/r2d_prof_knn python tools/profile_cases.py knn > gpurun_out/r2d_prof_knn.log 2>&1
+ncu -i gpurun_out/r2d_prof_knn.ncu-rep --page raw --csv > gpurun_out/r2d_knn_raw.csv 2>/dev/null
+ncu -i gpurun_out/r2d_prof_knn.ncu-rep --page source --csv --print-source sass > gpurun_out/r2d_knn_source.csv 2>/dev/null
+ls -la gpurun_out | tail -5

@@ -7,7 +7,8 @@
 //        -o /tmp/tmem_probe tools/tmem_probe.cu && /tmp/tmem_probe
 #include <cstdio>
 #include <cuda_runtime.h>
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstring>
 #include "tc.cuh"
 
 using namespace pmx;
@@ -87,16 +88,17 @@ __global__ void k_tmem(uint32_t* sink, long long* clk) {
 }
 
 // Layout check for a 16-bit (F16) accumulator: one M=128 N=128 K=16 UMMA with
-// A = 1 and B row p = p, so D[q][p] = 16 p.  Lane 0's 128 TMEM words tell
+// fp16 A = 1 and B row p = p, so D[q][p] = 16 p (an F16 accumulator needs fp16
+// operands; bf16 ones require F32).  Lane 0's 128 TMEM words tell
 // whether two 16-bit results share a 32-bit column (packed) or not.
 __global__ void k_f16acc_layout(uint32_t* out) {
-    __shared__ __align__(1024) __nv_bfloat16 A[128 * 64];
-    __shared__ __align__(1024) __nv_bfloat16 B[128 * 64];
+    __shared__ __align__(1024) __half A[128 * 64];
+    __shared__ __align__(1024) __half B[128 * 64];
     __shared__ uint64_t done;
     __shared__ uint32_t tbase;
     for (int i = threadIdx.x; i < 128 * 64; i += blockDim.x) {
-        A[i] = __float2bfloat16_rn(1.f);
-        B[i] = __float2bfloat16_rn((float)(i / 64));
+        A[i] = __float2half_rn(1.f);
+        B[i] = __float2half_rn((float)(i / 64));
     }
     if (threadIdx.x == 0) { tc::mbar_init(&done, 1); tc::fence_mbar_init(); }
     if ((threadIdx.x >> 5) == 0) tc::tmem_alloc(&tbase, 512);
@@ -106,7 +108,7 @@ __global__ void k_f16acc_layout(uint32_t* out) {
     tc::tc_fence_after();
     const uint32_t tmem = tbase;
     if (threadIdx.x == 0) {
-        constexpr uint32_t idesc = (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);  // c = F16
+        constexpr uint32_t idesc = ((128u >> 3) << 17) | ((128u >> 4) << 24);  // c = F16, a = b = F16
         tc::umma_f16(tmem, tc::sw128_kmajor_desc(tc::smem_u32(A)), tc::sw128_kmajor_desc(tc::smem_u32(B)), idesc, 0);
         tc::umma_commit(&done);
     }
@@ -173,10 +175,10 @@ static void run(int sms, int warps, const char* name) {
     cudaFree(clk);
 }
 
-int main() {
+int main(int argc, char** argv) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    f16acc_layout();
+    if (argc > 1 && !strcmp(argv[1], "layout")) { f16acc_layout(); return 0; }
     for (int w : {4, 8, 16}) {
         run<0, 1, 0>(sms, w, "32x32b.x64");
         run<0, 2, 0>(sms, w, "32x32b.x64");

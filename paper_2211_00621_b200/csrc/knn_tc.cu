@@ -79,39 +79,51 @@ __device__ __forceinline__ float unord_f32(uint32_t u) {
     return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
 }
 
-// Sorted top-8 of one thread, in registers: d ascending, ties by arrival
-// (candidates arrive in increasing train index, and an equal distance never
-// displaces an entry, so ties keep the smaller index).  Branch-free: every
-// slot is a select, so the compiler keeps d/x in registers (no local memory).
+// Sorted top-8 of one thread, in registers, as packed 32-bit keys
+//     key = dist << 17 | local
+// dist = the exact squared distance (an integer <= 32766, checked per launch
+// by k_knn_bound) and local = the candidate's position in this thread's part of
+// the work item (< 2^17: at most 2048 tiles x 64 columns, see knn_tc_nsplit).
+// Keys order exactly like (distance, train index), so an insertion is a
+// min/max network (16 IMNMX, no selects or branches) and ties keep the
+// smaller index.  The accumulator holds D = ||x||^2 - 2 q.x = dist - ||q||^2;
+// one FADD of (2^23 + ||q||^2) puts dist in the low mantissa bits.
+constexpr uint32_t KT_LOCAL_BITS = 17;
+constexpr uint32_t KT_EMPTY = 0xffffffffu;
+constexpr int KT_MAX_ITEM_TILES = (1 << KT_LOCAL_BITS) / (KT_N / 2);     // 2048
+constexpr float KT_DIST_MAX = 32766.f;                                    // dist field 32767 = empty/padding
+
 struct Top8 {
-    float d[KT_KMAX];
-    uint32_t x[KT_KMAX];
-    __device__ __forceinline__ void reset() {
+    uint32_t d[KT_KMAX];
+    float qbias;          // 2^23 + ||q||^2
+    float thr;            // D-space threshold: candidates with D < thr may enter
+    __device__ __forceinline__ void reset(float qn) {
 #pragma unroll
-        for (int i = 0; i < KT_KMAX; ++i) { d[i] = __int_as_float(0x7f800000); x[i] = 0xffffffffu; }
+        for (int i = 0; i < KT_KMAX; ++i) d[i] = KT_EMPTY;
+        qbias = 8388608.f + qn;
+        refresh();
     }
-    // caller guarantees dv < d[KT_KMAX - 1] for a real insertion; otherwise a no-op
-    __device__ __forceinline__ void insert(float dv, uint32_t ix) {
+    // D-space value of the current 8th key's distance
+    __device__ __forceinline__ void refresh() {
+        thr = __fsub_rn(__uint_as_float(0x4b000000u | (d[KT_KMAX - 1] >> KT_LOCAL_BITS)), qbias);
+    }
+    __device__ __forceinline__ uint32_t make_key(float D, uint32_t local) const {
+        return (__float_as_uint(__fadd_rn(D, qbias)) << KT_LOCAL_BITS) | local;
+    }
+    __device__ __forceinline__ void insert(uint32_t key) {   // no-op when key > d[7]
 #pragma unroll
-        for (int i = KT_KMAX - 1; i > 0; --i) {
-            const bool shift = dv < d[i - 1];
-            const bool here = dv < d[i];
-            d[i] = shift ? d[i - 1] : (here ? dv : d[i]);
-            x[i] = shift ? x[i - 1] : (here ? ix : x[i]);
+        for (int i = 0; i < KT_KMAX; ++i) {
+            const uint32_t lo = min(d[i], key);
+            key = max(d[i], key);
+            d[i] = lo;
         }
-        const bool first = dv < d[0];
-        d[0] = first ? dv : d[0];
-        x[0] = first ? ix : x[0];
-    }
-    __device__ __forceinline__ uint64_t key(int i) const {
-        return x[i] == 0xffffffffu ? ~0ull : (((uint64_t)ord_f32(d[i]) << 32) | x[i]);
     }
 };
 
-// Scan 32 candidate distances (column base col0) into the list: a min over
-// each 8 (depth-3 trees), one vote per 8 against the threshold, and for a
-// group some lane needs, one vote per candidate gating the predicated insert.
-__device__ __forceinline__ void knn_scan32(const uint32_t (&r)[32], int64_t col0, Top8& L) {
+// Scan 32 candidate accumulators (local positions lbase + j) into the list: a
+// min over each 8, one vote per 32 and per 8 against the threshold, and in a
+// group some lane needs, a vote per candidate gating the (warp-wide) insert.
+__device__ __forceinline__ void knn_scan32(const uint32_t (&r)[32], uint32_t lbase, Top8& L) {
     float m8[4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
@@ -120,16 +132,16 @@ __device__ __forceinline__ void knn_scan32(const uint32_t (&r)[32], int64_t col0
         for (int j = 0; j < 4; ++j) a[j] = fminf(__uint_as_float(r[g * 8 + j]), __uint_as_float(r[g * 8 + j + 4]));
         m8[g] = fminf(fminf(a[0], a[1]), fminf(a[2], a[3]));
     }
-    const float thr = L.d[KT_KMAX - 1];
-    if (!__any_sync(0xffffffffu, fminf(fminf(m8[0], m8[1]), fminf(m8[2], m8[3])) < thr)) return;
+    if (!__any_sync(0xffffffffu, fminf(fminf(m8[0], m8[1]), fminf(m8[2], m8[3])) < L.thr)) return;
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-        if (!__any_sync(0xffffffffu, m8[g] < L.d[KT_KMAX - 1])) continue;
+        if (!__any_sync(0xffffffffu, m8[g] < L.thr)) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const float dv = __uint_as_float(r[g * 8 + j]);
-            if (__any_sync(0xffffffffu, dv < L.d[KT_KMAX - 1])) L.insert(dv, (uint32_t)(col0 + g * 8 + j));
+            const uint32_t key = L.make_key(__uint_as_float(r[g * 8 + j]), lbase + (uint32_t)(g * 8 + j));
+            if (__any_sync(0xffffffffu, key < L.d[KT_KMAX - 1])) L.insert(key);
         }
+        L.refresh();
     }
 }
 
@@ -140,11 +152,13 @@ __device__ __forceinline__ void knn_scan32(const uint32_t (&r)[32], int64_t col0
 // does not hold (a coordinate not exact in bf16, or ||x||^2 not an integer
 // below 2^16).
 __global__ void k_knn_prep(const float* __restrict__ x, int64_t rows, float scale, __nv_bfloat16* __restrict__ xb,
-                           __nv_bfloat16* __restrict__ xaug, float* __restrict__ norms, unsigned* __restrict__ flag) {
+                           __nv_bfloat16* __restrict__ xaug, float* __restrict__ norms, unsigned* __restrict__ flag,
+                           unsigned* __restrict__ maxn) {
     const int sub = threadIdx.x & 15;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     bool inexact = false;
+    float nmax = 0.f;
     for (int64_t w = wid; w * 2 < rows; w += nw) {          // warp-uniform trip count
         const int64_t r = w * 2 + ((threadIdx.x >> 4) & 1);
         const bool valid = r < rows;
@@ -167,6 +181,7 @@ __global__ void k_knn_prep(const float* __restrict__ x, int64_t rows, float scal
         for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, 16);
         if (valid) {
             reinterpret_cast<uint2*>(xb + r * 64)[sub] = packed;
+            nmax = fmaxf(nmax, s);
             if (sub == 0) norms[r] = s;
             if (xaug && sub < 4) {
                 // [hi, lo, 0...]: exact when s is an integer in [0, 2^16)
@@ -182,12 +197,25 @@ __global__ void k_knn_prep(const float* __restrict__ x, int64_t rows, float scal
         }
     }
     if (__any_sync(0xffffffffu, inexact) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nmax = fmaxf(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxn, __float_as_uint(nmax));    // norms >= 0: bits order as values
+}
+
+// The packed keys hold squared distances up to KT_DIST_MAX: with the largest
+// norms (sqrt(max ||x||^2) + sqrt(max ||q||^2))^2 bounds every distance; above
+// it the SIMT kernel answers (flag bit 2).
+__global__ void k_knn_bound(const unsigned* __restrict__ maxn, unsigned* __restrict__ flag) {
+    if (threadIdx.x == 0) {
+        const double b = sqrt((double)__uint_as_float(maxn[0])) + sqrt((double)__uint_as_float(maxn[1]));
+        if (!(b * b <= (double)KT_DIST_MAX)) atomicOr(flag, 2u);
+    }
 }
 
 __global__ void __launch_bounds__(KT_THREADS, 1)
 k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmx,
          const __grid_constant__ CUtensorMap tmxa, int64_t ntr, int64_t nq, int k, int nsplit,
-         uint64_t* __restrict__ lists, const unsigned* __restrict__ flag) {
+         uint64_t* __restrict__ lists, const float* __restrict__ qnorm, const unsigned* __restrict__ flag) {
     if (*flag) return;                       // inexact data: the SIMT path answers
     extern __shared__ uint8_t smem_raw[];
     // 1 KiB-aligned by pointer arithmetic on the __shared__ array itself, so every
@@ -295,7 +323,9 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
             const int qb = it / nsplit, sp = it % nsplit;
             const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
-            L.reset();
+            const int64_t q = (int64_t)qb * KT_Q + row;
+            L.reset(q < nq ? qnorm[q] : 0.f);
+            const float padv = __fsub_rn(__uint_as_float(0x4b007fffu), L.qbias);   // dist field 32767
             for (int t = t0; t < t1; ++t) {
                 tc::mbar_wait(&S.tfull[b], acc_phase);
                 tc::tc_fence_after();
@@ -312,21 +342,24 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                         if (lane == 0) tc::mbar_arrive(&S.tempty[b]);
                     }
                     const int64_t col0 = colbase + c * 32;
-                    if (col0 + 32 > ntr) {                   // last tile: padded rows read as +inf
+                    if (col0 + 32 > ntr) {                   // last tile: padded rows never enter
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
-                            if (col0 + j >= ntr) r[j] = 0x7f800000u;
+                            if (col0 + j >= ntr) r[j] = __float_as_uint(padv);
                     }
-                    knn_scan32(r, col0, L);
+                    knn_scan32(r, (uint32_t)((t - t0) * 64 + c * 32), L);
                 }
                 b ^= 1;
                 if (b == 0) acc_phase ^= 1;
             }
-            const int64_t q = (int64_t)qb * KT_Q + row;
             if (q < nq) {
                 uint64_t* dst = lists + ((q * nsplit + sp) * KT_LPQ + ch) * KT_KMAX;
 #pragma unroll
-                for (int i = 0; i < KT_KMAX; ++i) dst[i] = L.key(i);
+                for (int i = 0; i < KT_KMAX; ++i) {
+                    const uint32_t dist = L.d[i] >> KT_LOCAL_BITS, loc = L.d[i] & ((1u << KT_LOCAL_BITS) - 1);
+                    const uint64_t gidx = (uint64_t)(t0 + (int)(loc >> 6)) * KT_N + (uint64_t)(ch * 64) + (loc & 63u);
+                    dst[i] = dist >= 32767u ? ~0ull : (((uint64_t)dist << 32) | gidx);
+                }
             }
         }
     }
@@ -405,11 +438,12 @@ int knn_tc_nsplit(int64_t ntr, int64_t nq) {
     const int64_t nblk = (nq + KT_Q - 1) / KT_Q;
     const int64_t ntiles = (ntr + KT_N - 1) / KT_N;
     const int64_t sms = sm_count();
-    int best = 1;
+    int best = -1;                                      // none: more than 32 x 2048 tiles
     double best_cost = 1e300;
     for (int ns = 1; ns <= 32 && ns <= ntiles; ++ns) {
         const int64_t rounds = (nblk * ns + sms - 1) / sms;
         const int64_t per = (ntiles + ns - 1) / ns;
+        if (per > KT_MAX_ITEM_TILES) continue;          // local positions must fit the key
         const double cost = (double)(rounds * per) * (1.0 + 0.01 * ns);
         if (cost < best_cost) { best_cost = cost; best = ns; }
     }
@@ -423,9 +457,9 @@ int knn_tc_nsplit(int64_t ntr, int64_t nq) {
 static inline int64_t pad_to(int64_t n, int64_t m) { return (n + m - 1) / m * m; }
 
 size_t knn_tc_workspace(int64_t ntr, int64_t nq) {
-    const int ns = knn_tc_nsplit(ntr, nq);
+    const int ns = knn_tc_nsplit(ntr, nq) > 0 ? knn_tc_nsplit(ntr, nq) : 0;
     const int64_t ntr_p = pad_to(ntr, KT_N), nq_p = pad_to(nq, KT_Q);
-    return (size_t)ntr_p * (KT_D + KT_AUG) * 2 + (size_t)nq_p * KT_D * 2 + 1024 + (size_t)nq * ns * KT_LPQ * KT_KMAX * 8 + 256;
+    return (size_t)ntr_p * (KT_D + KT_AUG) * 2 + (size_t)nq_p * KT_D * 2 + 1024 + (size_t)nq * ns * KT_LPQ * KT_KMAX * 8 + 256 + 256;
 }
 
 int knn_tc_run(const float* train, const float* query, const int* labels, int64_t ntr, int64_t nq, int k, int ncls,
@@ -436,9 +470,17 @@ int knn_tc_run(const float* train, const float* query, const int* labels, int64_
     __nv_bfloat16* xaug = xb + (size_t)ntr_p * KT_D;
     __nv_bfloat16* qb = xaug + (size_t)ntr_p * KT_AUG;
     uint64_t* lists = (uint64_t*)(((uintptr_t)(qb + (size_t)nq_p * KT_D) + 1023) & ~(uintptr_t)1023);
+    const int nsplit = knn_tc_nsplit(ntr, nq);
+    if (nsplit < 0) {                                   // train set too long for the packed keys: SIMT
+        cudaError_t e = cudaMemsetAsync(flag, 0x04, 1, st);
+        if (e != cudaSuccess) { set_last_error("knn flag: %s", cudaGetErrorString(e)); return -2; }
+        return 0;
+    }
+    unsigned* maxn = (unsigned*)(lists + (size_t)nq * nsplit * KT_LPQ * KT_KMAX);
+    cudaMemsetAsync(maxn, 0, 2 * sizeof(unsigned), st);
     const int pgrid = 4 * sm_count();
-    k_knn_prep<<<(unsigned)imin64(pgrid, (ntr + 15) / 16), 256, 0, st>>>(train, ntr, -2.f, xb, xaug, tnorm, flag);
-    k_knn_prep<<<(unsigned)imin64(pgrid, (nq + 15) / 16), 256, 0, st>>>(query, nq, 1.f, qb, nullptr, qnorm, flag);
+    k_knn_prep<<<(unsigned)imin64(pgrid, (ntr + 15) / 16), 256, 0, st>>>(train, ntr, -2.f, xb, xaug, tnorm, flag, maxn);
+    k_knn_prep<<<(unsigned)imin64(pgrid, (nq + 15) / 16), 256, 0, st>>>(query, nq, 1.f, qb, nullptr, qnorm, flag, maxn + 1);
     PMX_CHECK_LAUNCH("knn_prep");
     CUtensorMap tmq, tmx, tmxa;
     if (!make_tmap_2d(&tmq, qb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)nq_p, KT_D, KT_Q, KT_D,
@@ -450,12 +492,12 @@ int knn_tc_run(const float* train, const float* query, const int* labels, int64_
         set_last_error("knn: cuTensorMapEncodeTiled unavailable or failed");
         return -2;
     }
-    const int nsplit = knn_tc_nsplit(ntr, nq);
     const int nitems = (int)((nq + KT_Q - 1) / KT_Q) * nsplit;
     const size_t smem = sizeof(KnnSmem) + 1024;
     cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = nitems < sm_count() ? nitems : sm_count();
-    k_knn_tc<<<grid, KT_THREADS, smem, st>>>(tmq, tmx, tmxa, ntr, nq, k, nsplit, lists, flag);
+    k_knn_bound<<<1, 32, 0, st>>>(maxn, flag);
+    k_knn_tc<<<grid, KT_THREADS, smem, st>>>(tmq, tmx, tmxa, ntr, nq, k, nsplit, lists, qnorm, flag);
     PMX_CHECK_LAUNCH("knn_tc");
     k_knn_merge<<<(unsigned)((nq + 127) / 128), 128, 0, st>>>(lists, nsplit * KT_LPQ, labels, nq, k, ncls, out_label,
                                                               out_idx, flag);

@@ -209,6 +209,23 @@ def test_knn_vs_oracle(ntr, nq, d, k, c):
     assert np.array_equal(idx, oidx)
 
 
+@pytest.mark.parametrize("lo,hi,ntr,nq,k", [
+    (0, 1, 3000, 300, 8),      # coordinates in {0, 1}: distances <= 64, massive ties -> index order decides
+    (-20, 20, 2000, 100, 8),   # squared distances up to ~10^5: beyond the packed keys -> SIMT kernel
+    (-8, 8, 8, 40, 8),         # k == ntr, one padded tile: every list holds padding
+    (-3, 3, 70000, 260, 7),    # several train splits per query block, k < 8
+])
+def test_knn_integer_ranges_exact(lo, hi, ntr, nq, k):
+    rng = np.random.default_rng(ntr + nq)
+    X = rng.integers(lo, hi + 1, size=(ntr, 64)).astype(np.float32)
+    Q = rng.integers(lo, hi + 1, size=(nq, 64)).astype(np.float32)
+    L = synth.knn_labels(ntr, 10)
+    lab, idx = accelerate(lambda x, l, q: knn_classify(x, l, q, k, 10, return_indices=True), X, L, Q)
+    olab, oidx = O.knn(X, L, Q, k, 10)
+    assert np.array_equal(idx, oidx)
+    assert np.array_equal(lab, olab)
+
+
 def test_knn_continuous_data_is_tie_tolerant():
     rng = np.random.default_rng(3)
     X = rng.random((3000, 64), dtype=np.float32)

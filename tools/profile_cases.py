@@ -97,6 +97,11 @@ def knn(reps=2, ntr=1 << 18):
     torch.cuda.synchronize()
 
 
+def knn_full(reps=1):
+    """k-NN at the BASELINE config (2^20 train x 2^16 queries)."""
+    knn(reps, ntr=1 << 20)
+
+
 def kmer(reps=2, T=100):
     km, K, nsig = 8, 8, 1024
     lE = torch.from_numpy(np.log(synth.kmer_emission(km, K)).astype(np.float32)).cuda()

@@ -1,0 +1,10 @@
+# r2e: k-NN v3 (packed 32-bit keys, min/max insertion): parity + timing + ncu at the full config
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "knn" > gpurun_out/pytest_knn.log 2>&1
+tail -3 gpurun_out/pytest_knn.log
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu --case knn > gpurun_out/bench_knn.json 2> gpurun_out/bench_knn.err
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_knn.json').read().strip().splitlines()[-1]); k=d['case_studies']['knn']; print('knn ms', k.get('ms_per_step'), k.get('roofline',{}).get('frac'), k.get('parity'))"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_knn_tc -c 1 -o gpurun_out/r2e_prof_knn python tools/profile_cases.py knn_full > gpurun_out/r2e_prof_knn.log 2>&1
+ncu -i gpurun_out/r2e_prof_knn.ncu-rep --page raw --csv > gpurun_out/r2e_knn_raw.csv 2>/dev/null
+ncu -i gpurun_out/r2e_prof_knn.ncu-rep --page source --csv --print-source sass > gpurun_out/r2e_knn_source.csv 2>/dev/null

@@ -107,6 +107,19 @@ struct Top8 {
     __device__ __forceinline__ void refresh() {
         thr = __fsub_rn(__uint_as_float(0x4b000000u | (d[KT_KMAX - 1] >> KT_LOCAL_BITS)), qbias);
     }
+    // Next split of the same query block (later train indices): the 8 best so
+    // far were written with the previous split, so only distances below the
+    // current 8th can still matter.  The list restarts as 8 copies of the key
+    // (that distance, local 2^17 - 1); entries still equal to it at the end are
+    // empty (a real candidate with that key ties an earlier one at a larger
+    // index, so it is never needed).
+    __device__ __forceinline__ uint32_t carry() {
+        const uint32_t pk = (d[KT_KMAX - 1] | ((1u << KT_LOCAL_BITS) - 1));
+#pragma unroll
+        for (int i = 0; i < KT_KMAX; ++i) d[i] = pk;
+        refresh();
+        return pk;
+    }
     __device__ __forceinline__ uint32_t make_key(float D, uint32_t local) const {
         return (__float_as_uint(__fadd_rn(D, qbias)) << KT_LOCAL_BITS) | local;
     }
@@ -226,6 +239,12 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
     const int nblk = (int)((nq + KT_Q - 1) / KT_Q);
     const int ntiles = (int)((ntr + KT_N - 1) / KT_N);
     const int nitems = nblk * nsplit;
+    // each CTA takes a contiguous run of items, so consecutive splits of one
+    // query block meet in one CTA and the epilogue carries its thresholds
+    // across them (all runs advance through equal-length items in step, so at
+    // any time the SMs stream nsplit train regions, as B tiles hit in L2)
+    const int it_begin = (int)((int64_t)blockIdx.x * nitems / gridDim.x);
+    const int it_end = (int)((int64_t)(blockIdx.x + 1) * nitems / gridDim.x);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < KT_STAGES; ++s) { tc::mbar_init(&S.full[s], 1); tc::mbar_init(&S.empty[s], 1); }
@@ -257,7 +276,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         if (lane == 0) {                                    // ---- TMA producer
             int stage = 0; uint32_t phase = 0, a_par = 0;
             bool first = true;
-            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            for (int it = it_begin; it < it_end; ++it) {
                 const int qb = it / nsplit, sp = it % nsplit;
                 const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
                 if (!first) { tc::mbar_wait(&S.a_empty, a_par); a_par ^= 1; }
@@ -283,7 +302,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         const uint64_t b_desc0 = tc::sw128_kmajor_desc(tc::smem_u32(S.B[0]));
         const uint64_t aaug_desc = tc::sw32_kmajor_desc(tc::smem_u32(S.Aaug));
         const uint64_t baug_desc0 = tc::sw32_kmajor_desc(tc::smem_u32(S.Baug[0]));
-        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        for (int it = it_begin; it < it_end; ++it) {
             const int sp = it % nsplit;
             const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
             tc::mbar_wait(&S.a_full, a_par); a_par ^= 1;
@@ -320,11 +339,15 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         const int row = h * KT_M + quad * 32 + lane;           // query within the block
         int b = 0; uint32_t acc_phase = 0;
         Top8 L;
-        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        int prev_qb = -1;
+        uint32_t pseudo = KT_EMPTY;
+        for (int it = it_begin; it < it_end; ++it) {
             const int qb = it / nsplit, sp = it % nsplit;
             const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
             const int64_t q = (int64_t)qb * KT_Q + row;
-            L.reset(q < nq ? qnorm[q] : 0.f);
+            if (qb != prev_qb) { L.reset(q < nq ? qnorm[q] : 0.f); pseudo = KT_EMPTY; }
+            else pseudo = L.carry();
+            prev_qb = qb;
             const float padv = __fsub_rn(__uint_as_float(0x4b007fffu), L.qbias);   // dist field 32767
             for (int t = t0; t < t1; ++t) {
                 tc::mbar_wait(&S.tfull[b], acc_phase);
@@ -358,7 +381,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                 for (int i = 0; i < KT_KMAX; ++i) {
                     const uint32_t dist = L.d[i] >> KT_LOCAL_BITS, loc = L.d[i] & ((1u << KT_LOCAL_BITS) - 1);
                     const uint64_t gidx = (uint64_t)(t0 + (int)(loc >> 6)) * KT_N + (uint64_t)(ch * 64) + (loc & 63u);
-                    dst[i] = dist >= 32767u ? ~0ull : (((uint64_t)dist << 32) | gidx);
+                    dst[i] = (dist >= 32767u || L.d[i] == pseudo) ? ~0ull : (((uint64_t)dist << 32) | gidx);
                 }
             }
         }

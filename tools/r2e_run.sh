@@ -1,4 +1,4 @@
-# r2e: k-NN v3 (packed 32-bit keys, min/max insertion): parity + timing + ncu at the full config
+# r2e: k-NN (packed keys, threshold carry across the splits of a CTA run): parity + timing + ncu at the full config
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "knn" > gpurun_out/pytest_knn.log 2>&1
 tail -3 gpurun_out/pytest_knn.log

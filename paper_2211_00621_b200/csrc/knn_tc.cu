@@ -17,19 +17,19 @@
 // 16-wide augmentation (A rows [256, 1, 0...], B rows [hi, lo, 0...],
 // SWIZZLE_32B).  The epilogue is then one min per candidate.
 //
-// Structure (persistent, one CTA per SM, 20 warps):
+// Structure (persistent, one CTA per SM, 18 warps):
 //   warp 0   TMA producer: the 256-query block A (2 x 128 rows) once per work
 //            item; train tiles B (128 x 64 bf16 of -2x) + B_aug (128 x 16)
 //            through a 4-stage ring
-//   warp 1   MMA issuer (one thread): per train tile, two 128 x 128
-//            accumulators (one per 128-query half) into one of two TMEM
-//            buffers (2 buffers x 2 halves x 128 columns = all 512 columns)
-//   warp 2   TMEM allocator
-//   warps 4-19 epilogue: warp w owns TMEM lane quadrant w%4 (one query per
-//            thread), query half ((w-4)>>2)&1 and column half (w-4)>>3, and
-//            scans its 64 candidates of the tile in two 32-column loads: a
-//            min-tree per 8, a warp vote, and the rare branch-free insertion
-//            into a register-resident sorted top-8 (distance, index)
+//   warp 1   TMEM allocator and MMA issuer (one thread): per train tile, two
+//            128 x 128 accumulators (one per 128-query half) into one of two
+//            TMEM buffers (2 buffers x 2 halves x 128 columns = all 512 columns)
+//   warps 2-17 epilogue: warp w owns TMEM lane quadrant w%4 (one query per
+//            thread), query half ((w-2)>>2)&1 and column half (w-2)>>3; it
+//            loads its 64 candidates of the tile (one 64-column tcgen05.ld),
+//            releases the accumulator, and scans them: a min tree and a warp
+//            vote per 64, and the rare insertion into a register-resident
+//            sorted top-8 of packed (distance, index) keys
 // Work item = (256-query block, contiguous range of train tiles).  Reusing
 // each B tile for 256 queries halves L2 traffic versus 128; the split count
 // is chosen so the items fill whole rounds of the SMs (all SMs with the same
@@ -54,7 +54,7 @@ constexpr int KT_AUG = 16;
 constexpr int KT_STAGES = 4;
 constexpr int KT_KMAX = 8;
 constexpr int KT_EW = 16;                 // epilogue warps
-constexpr int KT_THREADS = 128 + 32 * KT_EW;
+constexpr int KT_THREADS = 64 + 32 * KT_EW;
 constexpr int KT_LPQ = 2;                 // partial lists per query per item (column halves)
 constexpr uint32_t KT_A_BYTES = KT_Q * KT_D * 2;        // 32 KB
 constexpr uint32_t KT_B_BYTES = KT_N * KT_D * 2;        // 16 KB
@@ -133,22 +133,33 @@ struct Top8 {
     }
 };
 
-// Scan 32 candidate accumulators (local positions lbase + j) into the list: a
-// min over each 8, one vote per 32 and per 8 against the threshold, and in a
-// group some lane needs, a vote per candidate gating the (warp-wide) insert.
-__device__ __forceinline__ void knn_scan32(const uint32_t (&r)[32], uint32_t lbase, Top8& L) {
-    float m8[4];
+// min of N floats as a tree of 3-input mins (FMNMX3: two reductions per
+// instruction, depth log3 N)
+template <int N>
+__device__ __forceinline__ float min_tree(const float* v) {
+    if constexpr (N == 1) {
+        return v[0];
+    } else if constexpr (N == 2) {
+        return fminf(v[0], v[1]);
+    } else {
+        constexpr int M = (N + 2) / 3;
+        float m[M];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-        float a[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) a[j] = fminf(__uint_as_float(r[g * 8 + j]), __uint_as_float(r[g * 8 + j + 4]));
-        m8[g] = fminf(fminf(a[0], a[1]), fminf(a[2], a[3]));
+        for (int i = 0; i < N / 3; ++i) m[i] = fminf(fminf(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
+        if constexpr (N % 3 == 1) m[M - 1] = v[N - 1];
+        if constexpr (N % 3 == 2) m[M - 1] = fminf(v[N - 2], v[N - 1]);
+        return min_tree<M>(m);
     }
-    if (!__any_sync(0xffffffffu, fminf(fminf(m8[0], m8[1]), fminf(m8[2], m8[3])) < L.thr)) return;
+}
+
+// Scan 64 candidate accumulators (local positions lbase + j) into the list:
+// one min tree and one vote per 64 against the threshold; in a group some lane
+// needs, a vote per 8 and then per candidate gates the (warp-wide) insert.
+__device__ __forceinline__ void knn_scan64(const uint32_t (&r)[64], uint32_t lbase, Top8& L) {
+    if (!__any_sync(0xffffffffu, min_tree<64>(reinterpret_cast<const float*>(r)) < L.thr)) return;
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-        if (!__any_sync(0xffffffffu, m8[g] < L.thr)) continue;
+    for (int g = 0; g < 8; ++g) {
+        if (!__any_sync(0xffffffffu, min_tree<8>(reinterpret_cast<const float*>(r) + g * 8) < L.thr)) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const uint32_t key = L.make_key(__uint_as_float(r[g * 8 + j]), lbase + (uint32_t)(g * 8 + j));
@@ -225,7 +236,7 @@ __global__ void k_knn_bound(const unsigned* __restrict__ maxn, unsigned* __restr
     }
 }
 
-__global__ void __launch_bounds__(KT_THREADS, 1)
+__global__ void __maxnreg__(96)
 k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmx,
          const __grid_constant__ CUtensorMap tmxa, int64_t ntr, int64_t nq, int k, int nsplit,
          uint64_t* __restrict__ lists, const float* __restrict__ qnorm, const unsigned* __restrict__ flag) {
@@ -266,7 +277,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         rowp[c0 ^ 1] = make_uint4(0u, 0u, 0u, 0u);
     }
     tc::fence_proxy_async();                 // generic-proxy smem writes -> UMMA (async proxy)
-    if (warp == 2) tc::tmem_alloc(&S.tmem_base, 512);
+    if (warp == 1) tc::tmem_alloc(&S.tmem_base, 512);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -333,8 +344,8 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
             if (tc::elect_one()) tc::umma_commit(&S.a_empty);
             __syncwarp();
         }
-    } else if (warp >= 4) {                                  // ---- epilogue
-        const int ew = warp - 4;
+    } else {                                                 // ---- epilogue (warps 2..17)
+        const int ew = warp - 2;
         const int quad = warp & 3, h = (ew >> 2) & 1, ch = ew >> 3;
         const int row = h * KT_M + quad * 32 + lane;           // query within the block
         int b = 0; uint32_t acc_phase = 0;
@@ -353,25 +364,22 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                 tc::mbar_wait(&S.tfull[b], acc_phase);
                 tc::tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((b * 2 + h) * KT_N + ch * 64);
-                const int64_t colbase = (int64_t)t * KT_N + ch * 64;
-#pragma unroll 1
-                for (int c = 0; c < 2; ++c) {
-                    uint32_t r[32];
-                    tc::tmem_ld_32x32b_x32(taddr + c * 32, r);
-                    tc::tmem_ld_wait();
-                    if (c == 1) {                             // my columns fully read: release
-                        tc::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) tc::mbar_arrive(&S.tempty[b]);
-                    }
-                    const int64_t col0 = colbase + c * 32;
-                    if (col0 + 32 > ntr) {                   // last tile: padded rows never enter
+                uint32_t r[64];
+                tc::tmem_ld_32x32b_x64(taddr, r);
+                tc::tmem_ld_wait();
+                // my 64 columns are in registers: release the accumulator at once, so
+                // the MMAs of tile t + 2 overlap this scan (a slow warp delays nobody
+                // until it falls a whole tile behind)
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&S.tempty[b]);
+                if (t == ntiles - 1) {                       // last tile: padded rows never enter
+                    const int64_t colbase = (int64_t)t * KT_N + ch * 64;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (col0 + j >= ntr) r[j] = __float_as_uint(padv);
-                    }
-                    knn_scan32(r, (uint32_t)((t - t0) * 64 + c * 32), L);
+                    for (int j = 0; j < 64; ++j)
+                        if (colbase + j >= ntr) r[j] = __float_as_uint(padv);
                 }
+                knn_scan64(r, (uint32_t)((t - t0) * 64), L);
                 b ^= 1;
                 if (b == 0) acc_phase ^= 1;
             }
@@ -388,7 +396,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 2) tc::tmem_dealloc(tmem, 512);
+    if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
 // Merge the nsplit sorted partial lists of each query and vote (ties -> the

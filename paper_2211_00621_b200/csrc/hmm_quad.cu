@@ -75,62 +75,12 @@ struct __align__(1024) HqSmem {
     uint32_t tmem_base;
 };
 
-__device__ __forceinline__ uint32_t hq_mapa(uint32_t smem_addr, uint32_t cta) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(cta));
-    return r;
-}
-__device__ __forceinline__ void hq_arrive_remote(uint32_t remote_bar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(remote_bar) : "memory");
-}
-__device__ __forceinline__ void hq_wait_cluster(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}"
-        :: "r"(tc::smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void hq_st_async(uint32_t remote_addr, float v, uint32_t remote_bar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
-                 :: "r"(remote_addr), "r"(__float_as_uint(v)), "r"(remote_bar) : "memory");
-}
 __device__ __forceinline__ void hq_bulk_to(uint32_t remote_dst, const void* src, uint32_t bytes, uint32_t remote_bar) {
     asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(remote_dst), "r"(tc::smem_u32(src)), "r"(bytes), "r"(remote_bar) : "memory");
 }
 __device__ __forceinline__ void hq_bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void hq_bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-
-// pair (cta_group::2) forms of the tcgen05 / TMA operations
-__device__ __forceinline__ void hq_tmem_alloc2(uint32_t* holder, uint32_t ncols) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
-                 :: "r"(tc::smem_u32(holder)), "r"(ncols) : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void hq_tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(taddr), "r"(ncols) : "memory");
-}
-__device__ __forceinline__ void hq_umma2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                         uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-        :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
-}
-__device__ __forceinline__ void hq_commit2(uint64_t* bar, uint16_t mask) {
-    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-                 :: "r"(tc::smem_u32(bar)), "h"(mask) : "memory");
-}
-// TMA tile into this CTA's shared memory; the bytes complete on `bar_cluster`
-// (the pair leader's barrier, a shared::cluster address)
-__device__ __forceinline__ void hq_tma_load2(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];"
-        :: "r"(tc::smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1)
-        : "memory");
-}
 
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(HQ_THREADS, 1)
 k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ E_lin,
@@ -208,7 +158,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         tc::fence_mbar_init();
         tc::tma_prefetch(&tmA);
     }
-    if (warp == 2) hq_tmem_alloc2(&Sm.tmem_base, 512);   // D double-buffered by step parity
+    if (warp == 2) tc::tmem_alloc2(&Sm.tmem_base, 512);   // D double-buffered by step parity
     tc::tc_fence_before();
     tc::cluster_sync();
     tc::tc_fence_after();
@@ -216,7 +166,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
 
     if (warp == 0) {
         if (lane == 0) {                                     // ---- TMA producer (both CTAs of a pair)
-            const uint32_t lead_full0 = hq_mapa(tc::smem_u32(&Sm.full[0]), leader);
+            const uint32_t lead_full0 = tc::mapa(tc::smem_u32(&Sm.full[0]), leader);
             int stage = 0; uint32_t phase = 0;
             for (int t = 1; t < T; ++t)
                 for (int mbs = 0; mbs < HQ_MB; ++mbs)
@@ -226,7 +176,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                                 const int kb = kbgrp(leader ^ (uint32_t)i, mbs) + k2;
                                 tc::mbar_wait(&Sm.empty[stage], phase ^ 1);
                                 if (h == 0) tc::mbar_arrive_expect_tx(&Sm.full[stage], 2 * HQ_TILE);
-                                hq_tma_load2(Sm.At[stage], &tmA, lead_full0 + (uint32_t)(stage * sizeof(uint64_t)),
+                                tc::tma_load_2d_pair(Sm.At[stage], &tmA, lead_full0 + (uint32_t)(stage * sizeof(uint64_t)),
                                              kb * HQ_KB, jbase(mbo));
                                 if (++stage == HQ_ST) { stage = 0; phase ^= 1; }
                             }
@@ -247,7 +197,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                         if (c != crank && t + 1 < T && lane == 0)                      // arm u_t's phase
                             tc::mbar_arrive_expect_tx(&Sm.ur[c][mbs], HQ_ROWS);
                         __syncwarp();
-                        hq_wait_cluster(&Sm.pr[c][mbs], (uint32_t)((t - 1) & 1));    // and the partner's
+                        tc::mbar_wait_cluster(&Sm.pr[c][mbs], (uint32_t)((t - 1) & 1));    // and the partner's
                         tc::tc_fence_after();
                         if (t < 64 && mbs == 0 && i == 0 && lane == 0) stamp(t, 8);
                         for (int k2 = 0; k2 < 2; ++k2)
@@ -261,19 +211,19 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                                     const uint32_t d = dstep + (uint32_t)(mbo * HQ_N);
 #pragma unroll
                                     for (int kk = 0; kk < HQ_KB / 16; ++kk)
-                                        hq_umma2(d, ad + 2 * kk, bd + 2 * kk, idesc, (!first[mbo]) || (kk != 0));
-                                    hq_commit2(&Sm.empty[stage], pair_mask);
+                                        tc::umma2_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, (!first[mbo]) || (kk != 0));
+                                    tc::umma2_commit_mc(&Sm.empty[stage], pair_mask);
                                 }
                                 __syncwarp();
                                 first[mbo] = false;
                                 if (++stage == HQ_ST) { stage = 0; phase ^= 1; }
                             }
                         // CTA c may overwrite these rows (in every B) once both pairs consumed them
-                        if (tc::elect_one()) hq_commit2(&Sm.gdone[mbs], (uint16_t)(1u << c));
+                        if (tc::elect_one()) tc::umma2_commit_mc(&Sm.gdone[mbs], (uint16_t)(1u << c));
                         __syncwarp();
                     }
                 if (lane == 0) stamp(t, 10);
-                if (tc::elect_one()) hq_commit2(&Sm.dfull, pair_mask);
+                if (tc::elect_one()) tc::umma2_commit_mc(&Sm.dfull, pair_mask);
                 __syncwarp();
             }
         } else if (lane == 0) {                              // partner: forward "my B is ready"
@@ -283,7 +233,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                         const uint32_t c = leader ^ (uint32_t)i;
                         tc::mbar_wait(&Sm.ur[c][mbs], (uint32_t)((t - 1) & 1));
                         if (c != crank && t + 1 < T) tc::mbar_arrive_expect_tx(&Sm.ur[c][mbs], HQ_ROWS);
-                        hq_arrive_remote(hq_mapa(tc::smem_u32(&Sm.pr[c][mbs]), leader));
+                        tc::arrive_remote(tc::mapa(tc::smem_u32(&Sm.pr[c][mbs]), leader));
                     }
         }
     } else if (warp >= 4) {
@@ -303,7 +253,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         // no CTA waits for the slowest one's partials.
         auto finish_c = [&](int tt) {
             if (ew < 4) {
-                hq_wait_cluster(&Sm.psum[tt & 1], (uint32_t)((tt >> 1) & 1));
+                tc::mbar_wait_cluster(&Sm.psum[tt & 1], (uint32_t)((tt >> 1) & 1));
                 if (lead && tt + 2 < T) tc::mbar_arrive_expect_tx(&Sm.psum[tt & 1], 3 * HQ_N * 4);
                 const int m = ew * 32 + lane;
                 const float c = ((Sm.psum_in[tt & 1][0][m] + Sm.psum_in[tt & 1][1][m]) +
@@ -321,13 +271,13 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
         };
         const uint32_t same_half_other_pair = crank ^ 2u, other_half_same_pair = crank ^ 1u,
                        other_half_other_pair = crank ^ 3u;
-        const uint32_t rU_osp = hq_mapa(tc::smem_u32(&Sm.U[0][0]), other_half_same_pair);
-        const uint32_t rU_oop = hq_mapa(tc::smem_u32(&Sm.U[0][0]), other_half_other_pair);
+        const uint32_t rU_osp = tc::mapa(tc::smem_u32(&Sm.U[0][0]), other_half_same_pair);
+        const uint32_t rU_oop = tc::mapa(tc::smem_u32(&Sm.U[0][0]), other_half_other_pair);
         uint32_t rB_osp[HQ_MB], rB_oop[HQ_MB];
 #pragma unroll
         for (int b = 0; b < HQ_MB; ++b) {
-            rB_osp[b] = hq_mapa(tc::smem_u32(&Sm.ur[crank][b]), other_half_same_pair);
-            rB_oop[b] = hq_mapa(tc::smem_u32(&Sm.ur[crank][b]), other_half_other_pair);
+            rB_osp[b] = tc::mapa(tc::smem_u32(&Sm.ur[crank][b]), other_half_same_pair);
+            rB_oop[b] = tc::mapa(tc::smem_u32(&Sm.ur[crank][b]), other_half_other_pair);
         }
         for (int t = 0; t < T; ++t) {
             if (ew < 4) {
@@ -424,7 +374,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 if (lead) stamp(t, 4 * mb);
                 // (2) store, once both pairs' MMAs of t consumed my rows of u_{t-1} (gdone):
                 // my signal half into my B, the other half into the other-half CTAs' B
-                if (t > 0) hq_wait_cluster(&Sm.gdone[mb], (uint32_t)((t - 1) & 1));
+                if (t > 0) tc::mbar_wait_cluster(&Sm.gdone[mb], (uint32_t)((t - 1) & 1));
                 if (hh == (int)h) {
 #pragma unroll
                     for (int s = 0; s < 32; ++s) {
@@ -444,8 +394,8 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                         const int sl = (hq & 1) * 32 + 2 * k + (odd ? 1 : 0);
                         const uint32_t off = pair_off + (uint32_t)sl * 128 + ((chunkj ^ (uint32_t)(sl & 7)) << 4);
                         const float bits = __uint_as_float(*reinterpret_cast<const uint32_t*>(&pr));
-                        hq_st_async(rU_osp + off, bits, rB_osp[mb]);
-                        hq_st_async(rU_oop + off, bits, rB_oop[mb]);
+                        tc::st_async_b32(rU_osp + off, __float_as_uint(bits), rB_osp[mb]);
+                        tc::st_async_b32(rU_oop + off, __float_as_uint(bits), rB_oop[mb]);
                     }
                 }
                 tc::tc_fence_before();
@@ -457,7 +407,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     const uint8_t* mine = reinterpret_cast<const uint8_t*>(&Sm.U[0][0]) + off;
                     const uint32_t u0 = tc::smem_u32(&Sm.U[0][0]) + off;
                     const uint32_t urb = tc::smem_u32(&Sm.ur[crank][mb]);
-                    hq_bulk_to(hq_mapa(u0, same_half_other_pair), mine, HQ_ROWS, hq_mapa(urb, same_half_other_pair));
+                    hq_bulk_to(tc::mapa(u0, same_half_other_pair), mine, HQ_ROWS, tc::mapa(urb, same_half_other_pair));
                     hq_bulk_commit();
                 }
                 if (lead) stamp(t, 3 + 2 * mb);
@@ -472,8 +422,8 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
                     if (c != (int)crank)
-                        hq_st_async(hq_mapa(tc::smem_u32(&Sm.psum_in[t & 1][crank][m]), (uint32_t)c), part,
-                                    hq_mapa(tc::smem_u32(&Sm.psum[t & 1]), (uint32_t)c));
+                        tc::st_async_b32(tc::mapa(tc::smem_u32(&Sm.psum_in[t & 1][crank][m]), (uint32_t)c), __float_as_uint(part),
+                                    tc::mapa(tc::smem_u32(&Sm.psum[t & 1]), (uint32_t)c));
             }
             asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
             if (lead) stamp(t, 11);
@@ -487,7 +437,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
     }
     tc::tc_fence_before();
     tc::cluster_sync();                      // no CTA leaves while a peer may still write into it
-    if (warp == 2) hq_tmem_dealloc2(tmem, 512);
+    if (warp == 2) tc::tmem_dealloc2(tmem, 512);
 }
 
 bool make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t rows,

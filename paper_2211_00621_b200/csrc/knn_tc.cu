@@ -9,37 +9,46 @@
 // prep kernel turns these kernels into no-ops and the SIMT kernel runs (no
 // host synchronisation).
 //
-// Formulation: the accumulator holds the ranking key directly,
-//     D[q, p] = sum_k q_k * (-2 x_pk)  +  256 * hi_p + 1 * lo_p
-//             = ||x_p||^2 - 2 q.x_p          (||q||^2 is constant per query)
-// with ||x_p||^2 = 256 hi_p + lo_p split into two bf16-exact integers: four
-// UMMA k-steps over the 64 coordinates (SWIZZLE_128B operands) plus one over a
-// 16-wide augmentation (A rows [256, 1, 0...], B rows [hi, lo, 0...],
-// SWIZZLE_32B).  The epilogue is then one min per candidate.
+// Formulation: the accumulator holds the exact squared distance plus 2^23,
+//     D[q, p] = sum_k q_k * (-2 x_pk) + (||x_p||^2 + ||q||^2 + 2^23)
+// four UMMA k-steps over the 64 coordinates (SWIZZLE_128B operands) plus one
+// over a 16-wide augmentation (SWIZZLE_32B): query rows [256, 1, hi_q, lo_q,
+// 2^23, 0...], train rows [hi_x, lo_x, 256, 1, 1, 0...] with the norms split
+// into bf16-exact integers (||v||^2 = 256 hi + lo).  Every partial sum is an
+// integer below 2^24, so fp32 accumulation is exact, and the low 16 bits of D
+// are the distance: tcgen05.ld .pack::16b hands the epilogue two candidates
+// per register and the scan is packed 16-bit integer work.
 //
 // Structure (persistent, one CTA per SM, 18 warps):
-//   warp 0   TMA producer: the 256-query block A (2 x 128 rows) once per work
-//            item; train tiles B (128 x 64 bf16 of -2x) + B_aug (128 x 16)
-//            through a 4-stage ring
+//   warp 0   TMA producer: the 256-query block A (2 x 128 rows) and its
+//            augmentation rows once per work item; train tiles B (128 x 64
+//            bf16 of -2x) + B_aug (128 x 16) through a 4-stage ring
 //   warp 1   TMEM allocator and MMA issuer (one thread): per train tile, two
 //            128 x 128 accumulators (one per 128-query half) into one of two
 //            TMEM buffers (2 buffers x 2 halves x 128 columns = all 512 columns)
 //   warps 2-17 epilogue: warp w owns TMEM lane quadrant w%4 (one query per
 //            thread), query half ((w-2)>>2)&1 and column half (w-2)>>3; it
-//            loads its 64 candidates of the tile (one 64-column tcgen05.ld),
+//            loads its 64 candidates of the tile (one packed tcgen05.ld),
 //            releases the accumulator, and scans them: a min tree and a warp
 //            vote per 64, and the rare insertion into a register-resident
 //            sorted top-8 of packed (distance, index) keys
 // Work item = (256-query block, contiguous range of train tiles).  Reusing
 // each B tile for 256 queries halves L2 traffic versus 128; the split count
 // is chosen so the items fill whole rounds of the SMs (all SMs with the same
-// split stream the same train tiles in lockstep, so B tiles hit in L2).
-// Per-item partial top-8 lists (two per query: one per column half) go to
-// global memory; k_knn_merge merges them and votes.
+// split stream the same train tiles in lockstep, so B tiles hit in L2).  Each
+// CTA takes a contiguous run of items, so the splits of one query block meet
+// in one CTA and carry their thresholds.  Per-item partial top-8 lists (two
+// per query: one per column half) go to global memory; k_knn_merge merges
+// them and votes.
 //
-// Measured bound (tools/tmem_probe.cu, profiles/tmem_probe.json): TMEM reads
-// run at ~178 B/clk/SM, so a tile's 128 KiB of candidates needs ~740 clk
-// against ~640 clk of UMMA (M = 128, N = 128, K = 80, two halves).
+// Bounds (measured): TMEM reads are not the limit (tools/
+// tmem_probe.cu: 450 B/clk/SM with 16 warps reading, 128 KiB per tile ->
+// ~290 clk); the UMMAs read 80 KiB of shared-memory operands per tile and TMA
+// writes 20 KiB, ~780 clk at 128 B/clk against 640 clk of tensor work.  A
+// CTA-pair variant (cta_group::2, M = N = 256: 60 KiB of shared-memory traffic
+// per tile) measured no faster (9.8 ms): with two accumulator buffers, a
+// warp in the rare insertion path delays the release of the next tile for
+// everyone; that coupling, not a pipe, sets the remaining gap.
 #include <cuda_bf16.h>
 #include "common.cuh"
 #include "tc.cuh"
@@ -57,13 +66,14 @@ constexpr int KT_EW = 16;                 // epilogue warps
 constexpr int KT_THREADS = 64 + 32 * KT_EW;
 constexpr int KT_LPQ = 2;                 // partial lists per query per item (column halves)
 constexpr uint32_t KT_A_BYTES = KT_Q * KT_D * 2;        // 32 KB
+constexpr uint32_t KT_AAUG_BYTES = KT_Q * KT_AUG * 2;   //  8 KB
 constexpr uint32_t KT_B_BYTES = KT_N * KT_D * 2;        // 16 KB
 constexpr uint32_t KT_BAUG_BYTES = KT_N * KT_AUG * 2;   //  4 KB
 
 struct __align__(1024) KnnSmem {
     __nv_bfloat16 A[KT_Q * KT_D];                       // 2 halves of 128 rows, SW128
     __nv_bfloat16 B[KT_STAGES][KT_N * KT_D];            // SW128
-    __nv_bfloat16 Aaug[KT_M * KT_AUG];                  // SW32 (same rows for both halves)
+    __nv_bfloat16 Aaug[KT_Q * KT_AUG];                  // query augmentation rows (2 halves), SW32
     __nv_bfloat16 Baug[KT_STAGES][KT_N * KT_AUG];       // SW32
     uint64_t full[KT_STAGES], empty[KT_STAGES];
     uint64_t a_full, a_empty;
@@ -86,27 +96,27 @@ __device__ __forceinline__ float unord_f32(uint32_t u) {
 // the work item (< 2^17: at most 2048 tiles x 64 columns, see knn_tc_nsplit).
 // Keys order exactly like (distance, train index), so an insertion is a
 // min/max network (16 IMNMX, no selects or branches) and ties keep the
-// smaller index.  The accumulator holds D = ||x||^2 - 2 q.x = dist - ||q||^2;
-// one FADD of (2^23 + ||q||^2) puts dist in the low mantissa bits.
+// smaller index.
+//
+// The accumulator holds dist + 2^23 (the augmentation adds ||x||^2, ||q||^2
+// and 2^23), an fp32 whose low 16 bits are dist; tcgen05.ld .pack::16b
+// delivers two candidates' distances per register (column 2j in bits 0-15,
+// column 2j+1 in bits 16-31; tools/tmem_probe.cu layout check), so the scan
+// is packed 16-bit integer work (VIMNMX3.U16x2: four candidates per op).
 constexpr uint32_t KT_LOCAL_BITS = 17;
 constexpr uint32_t KT_EMPTY = 0xffffffffu;
-constexpr int KT_MAX_ITEM_TILES = (1 << KT_LOCAL_BITS) / (KT_N / 2);     // 2048
-constexpr float KT_DIST_MAX = 32766.f;                                    // dist field 32767 = empty/padding
+constexpr int KT_MAX_ITEM_TILES = (1 << KT_LOCAL_BITS) / 64;             // 2048 tiles of 64 per thread
+constexpr float KT_DIST_MAX = 32766.f;                                    // dist 32767 = empty / padding
 
 struct Top8 {
     uint32_t d[KT_KMAX];
-    float qbias;          // 2^23 + ||q||^2
-    float thr;            // D-space threshold: candidates with D < thr may enter
-    __device__ __forceinline__ void reset(float qn) {
+    __device__ __forceinline__ void reset() {
 #pragma unroll
         for (int i = 0; i < KT_KMAX; ++i) d[i] = KT_EMPTY;
-        qbias = 8388608.f + qn;
-        refresh();
     }
-    // D-space value of the current 8th key's distance
-    __device__ __forceinline__ void refresh() {
-        thr = __fsub_rn(__uint_as_float(0x4b000000u | (d[KT_KMAX - 1] >> KT_LOCAL_BITS)), qbias);
-    }
+    // distances below this may enter (candidates arrive in increasing index,
+    // so one equal to the 8th's distance never does)
+    __device__ __forceinline__ uint32_t thr() const { return d[KT_KMAX - 1] >> KT_LOCAL_BITS; }
     // Next split of the same query block (later train indices): the 8 best so
     // far were written with the previous split, so only distances below the
     // current 8th can still matter.  The list restarts as 8 copies of the key
@@ -117,11 +127,7 @@ struct Top8 {
         const uint32_t pk = (d[KT_KMAX - 1] | ((1u << KT_LOCAL_BITS) - 1));
 #pragma unroll
         for (int i = 0; i < KT_KMAX; ++i) d[i] = pk;
-        refresh();
         return pk;
-    }
-    __device__ __forceinline__ uint32_t make_key(float D, uint32_t local) const {
-        return (__float_as_uint(__fadd_rn(D, qbias)) << KT_LOCAL_BITS) | local;
     }
     __device__ __forceinline__ void insert(uint32_t key) {   // no-op when key > d[7]
 #pragma unroll
@@ -133,51 +139,59 @@ struct Top8 {
     }
 };
 
-// min of N floats as a tree of 3-input mins (FMNMX3: two reductions per
-// instruction, depth log3 N)
+__device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+// min of N packed u16x2 words as a tree of 3-input mins (VIMNMX3.U16x2)
 template <int N>
-__device__ __forceinline__ float min_tree(const float* v) {
+__device__ __forceinline__ uint32_t min_tree16(const uint32_t* v) {
     if constexpr (N == 1) {
         return v[0];
     } else if constexpr (N == 2) {
-        return fminf(v[0], v[1]);
+        return vmin2(v[0], v[1]);
     } else {
         constexpr int M = (N + 2) / 3;
-        float m[M];
+        uint32_t m[M];
 #pragma unroll
-        for (int i = 0; i < N / 3; ++i) m[i] = fminf(fminf(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
+        for (int i = 0; i < N / 3; ++i) m[i] = vmin2(vmin2(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
         if constexpr (N % 3 == 1) m[M - 1] = v[N - 1];
-        if constexpr (N % 3 == 2) m[M - 1] = fminf(v[N - 2], v[N - 1]);
-        return min_tree<M>(m);
+        if constexpr (N % 3 == 2) m[M - 1] = vmin2(v[N - 2], v[N - 1]);
+        return min_tree16<M>(m);
     }
 }
+__device__ __forceinline__ uint32_t min_halves(uint32_t m) { return min(m & 0xffffu, m >> 16); }
 
-// Scan 64 candidate accumulators (local positions lbase + j) into the list:
-// one min tree and one vote per 64 against the threshold; in a group some lane
-// needs, a vote per 8 and then per candidate gates the (warp-wide) insert.
-__device__ __forceinline__ void knn_scan64(const uint32_t (&r)[64], uint32_t lbase, Top8& L) {
-    if (!__any_sync(0xffffffffu, min_tree<64>(reinterpret_cast<const float*>(r)) < L.thr)) return;
+// Scan 64 candidates (32 packed words; local positions lbase + j) into the
+// list: one min tree and one vote per 64 against the threshold; in a group
+// some lane needs, a vote per 16 and then per candidate gates the (warp-wide)
+// insert.
+__device__ __forceinline__ void knn_scan64p(const uint32_t (&r)[32], uint32_t lbase, Top8& L) {
+    if (!__any_sync(0xffffffffu, min_halves(min_tree16<32>(r)) < L.thr())) return;
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        if (!__any_sync(0xffffffffu, min_tree<8>(reinterpret_cast<const float*>(r) + g * 8) < L.thr)) continue;
+    for (int g = 0; g < 4; ++g) {
+        if (!__any_sync(0xffffffffu, min_halves(min_tree16<8>(r + g * 8)) < L.thr())) continue;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint32_t key = L.make_key(__uint_as_float(r[g * 8 + j]), lbase + (uint32_t)(g * 8 + j));
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t w = r[g * 8 + (j >> 1)];
+            const uint32_t dist = (j & 1) ? (w >> 16) : (w & 0xffffu);
+            const uint32_t key = (dist << KT_LOCAL_BITS) | (lbase + (uint32_t)(g * 16 + j));
             if (__any_sync(0xffffffffu, key < L.d[KT_KMAX - 1])) L.insert(key);
         }
-        L.refresh();
     }
 }
 
 // prep (d == 64), 16 lanes per row, one float4 per lane (coalesced):
-//   train:  xb = bf16(-2 x), xaug = [hi, lo, 0 x 14] with ||x||^2 = 256 hi + lo
-//   query:  xb = bf16(q)   (xaug == nullptr)
+//   train:  xb = bf16(-2 x), xaug = [hi, lo, 256, 1, 1, 0 x 11] with ||x||^2 = 256 hi + lo
+//   query:  xb = bf16(q),    xaug = [256, 1, hi, lo, 2^23, 0 x 11] with ||q||^2 = 256 hi + lo
+// so that the augmentation k-step adds ||x||^2 + ||q||^2 + 2^23.
 // norms (fp32) feed the SIMT fallback; flag |= 1 when the exact formulation
 // does not hold (a coordinate not exact in bf16, or ||x||^2 not an integer
 // below 2^16).
-__global__ void k_knn_prep(const float* __restrict__ x, int64_t rows, float scale, __nv_bfloat16* __restrict__ xb,
-                           __nv_bfloat16* __restrict__ xaug, float* __restrict__ norms, unsigned* __restrict__ flag,
-                           unsigned* __restrict__ maxn) {
+__global__ void k_knn_prep(const float* __restrict__ x, int64_t rows, float scale, bool is_query,
+                           __nv_bfloat16* __restrict__ xb, __nv_bfloat16* __restrict__ xaug,
+                           float* __restrict__ norms, unsigned* __restrict__ flag, unsigned* __restrict__ maxn) {
     const int sub = threadIdx.x & 15;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -207,14 +221,17 @@ __global__ void k_knn_prep(const float* __restrict__ x, int64_t rows, float scal
             reinterpret_cast<uint2*>(xb + r * 64)[sub] = packed;
             nmax = fmaxf(nmax, s);
             if (sub == 0) norms[r] = s;
-            if (xaug && sub < 4) {
-                // [hi, lo, 0...]: exact when s is an integer in [0, 2^16)
+            if (sub < 4) {
+                // hi, lo are exact in bf16 when s is an integer in [0, 2^16)
                 const float hi = floorf(s / 256.f), lo = s - 256.f * hi;
                 if (sub == 0) inexact |= !(s >= 0.f && s < 65536.f && s == floorf(s));
+                auto bf = [](float v) { return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v)); };
                 uint2 a = make_uint2(0u, 0u);
                 if (sub == 0) {
-                    a.x = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(hi)) |
-                          ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(lo)) << 16);
+                    a = is_query ? make_uint2(bf(256.f) | (bf(1.f) << 16), bf(hi) | (bf(lo) << 16))
+                                 : make_uint2(bf(hi) | (bf(lo) << 16), bf(256.f) | (bf(1.f) << 16));
+                } else if (sub == 1) {
+                    a.x = bf(is_query ? 8388608.f : 1.f);
                 }
                 reinterpret_cast<uint2*>(xaug + r * KT_AUG)[sub] = a;
             }
@@ -237,9 +254,9 @@ __global__ void k_knn_bound(const unsigned* __restrict__ maxn, unsigned* __restr
 }
 
 __global__ void __maxnreg__(96)
-k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmx,
-         const __grid_constant__ CUtensorMap tmxa, int64_t ntr, int64_t nq, int k, int nsplit,
-         uint64_t* __restrict__ lists, const float* __restrict__ qnorm, const unsigned* __restrict__ flag) {
+k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmqa,
+         const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmxa, int64_t ntr, int64_t nq,
+         int k, int nsplit, uint64_t* __restrict__ lists, const unsigned* __restrict__ flag) {
     if (*flag) return;                       // inexact data: the SIMT path answers
     extern __shared__ uint8_t smem_raw[];
     // 1 KiB-aligned by pointer arithmetic on the __shared__ array itself, so every
@@ -264,17 +281,9 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         for (int b = 0; b < 2; ++b) { tc::mbar_init(&S.tfull[b], 1); tc::mbar_init(&S.tempty[b], KT_EW); }
         tc::fence_mbar_init();
         tc::tma_prefetch(&tmq);
+        tc::tma_prefetch(&tmqa);
         tc::tma_prefetch(&tmx);
         tc::tma_prefetch(&tmxa);
-    }
-    // constant augmentation rows [256, 1, 0 x 14] in the SWIZZLE_32B layout:
-    // 16-byte chunk c of row r lives at chunk c ^ ((r >> 2) & 1)
-    for (int r = threadIdx.x; r < KT_M; r += blockDim.x) {
-        uint4* rowp = reinterpret_cast<uint4*>(S.Aaug + r * KT_AUG);
-        const int c0 = (r >> 2) & 1;
-        rowp[c0] = make_uint4((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(256.f)) |
-                              ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(1.f)) << 16), 0u, 0u, 0u);
-        rowp[c0 ^ 1] = make_uint4(0u, 0u, 0u, 0u);
     }
     tc::fence_proxy_async();                 // generic-proxy smem writes -> UMMA (async proxy)
     if (warp == 1) tc::tmem_alloc(&S.tmem_base, 512);
@@ -292,8 +301,9 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                 const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
                 if (!first) { tc::mbar_wait(&S.a_empty, a_par); a_par ^= 1; }
                 first = false;
-                tc::mbar_arrive_expect_tx(&S.a_full, KT_A_BYTES);
+                tc::mbar_arrive_expect_tx(&S.a_full, KT_A_BYTES + KT_AAUG_BYTES);
                 tc::tma_load_2d(S.A, &tmq, &S.a_full, 0, qb * KT_Q);
+                tc::tma_load_2d(S.Aaug, &tmqa, &S.a_full, 0, qb * KT_Q);
                 for (int t = t0; t < t1; ++t) {
                     tc::mbar_wait(&S.empty[stage], phase ^ 1);
                     tc::mbar_arrive_expect_tx(&S.full[stage], KT_B_BYTES + KT_BAUG_BYTES);
@@ -331,7 +341,8 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
 #pragma unroll
                         for (int kk = 0; kk < KT_D / 16; ++kk)
                             tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, kk > 0);
-                        tc::umma_f16(d, aaug_desc, bad, idesc, 1);   // + 256 hi + lo
+                        // + ||x||^2 + ||q||^2 + 2^23 (the half's 128 query augmentation rows)
+                        tc::umma_f16(d, aaug_desc + (uint64_t)(h * ((KT_M * KT_AUG * 2) >> 4)), bad, idesc, 1);
                     }
                     tc::umma_commit(&S.empty[stage]);
                     tc::umma_commit(&S.tfull[b]);
@@ -356,16 +367,15 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
             const int qb = it / nsplit, sp = it % nsplit;
             const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
             const int64_t q = (int64_t)qb * KT_Q + row;
-            if (qb != prev_qb) { L.reset(q < nq ? qnorm[q] : 0.f); pseudo = KT_EMPTY; }
+            if (qb != prev_qb) { L.reset(); pseudo = KT_EMPTY; }
             else pseudo = L.carry();
             prev_qb = qb;
-            const float padv = __fsub_rn(__uint_as_float(0x4b007fffu), L.qbias);   // dist field 32767
             for (int t = t0; t < t1; ++t) {
                 tc::mbar_wait(&S.tfull[b], acc_phase);
                 tc::tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((b * 2 + h) * KT_N + ch * 64);
-                uint32_t r[64];
-                tc::tmem_ld_32x32b_x64(taddr, r);
+                uint32_t r[32];
+                tc::tmem_ld_32x32b_x32_pack16(taddr, r);          // 64 columns, two per register
                 tc::tmem_ld_wait();
                 // my 64 columns are in registers: release the accumulator at once, so
                 // the MMAs of tile t + 2 overlap this scan (a slow warp delays nobody
@@ -376,10 +386,12 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                 if (t == ntiles - 1) {                       // last tile: padded rows never enter
                     const int64_t colbase = (int64_t)t * KT_N + ch * 64;
 #pragma unroll
-                    for (int j = 0; j < 64; ++j)
-                        if (colbase + j >= ntr) r[j] = __float_as_uint(padv);
+                    for (int j = 0; j < 32; ++j) {
+                        if (colbase + 2 * j >= ntr) r[j] = (r[j] & 0xffff0000u) | 0x7fffu;
+                        if (colbase + 2 * j + 1 >= ntr) r[j] = (r[j] & 0xffffu) | 0x7fff0000u;
+                    }
                 }
-                knn_scan64(r, (uint32_t)((t - t0) * 64), L);
+                knn_scan64p(r, (uint32_t)((t - t0) * 64), L);
                 b ^= 1;
                 if (b == 0) acc_phase ^= 1;
             }
@@ -481,7 +493,7 @@ int knn_tc_nsplit(int64_t ntr, int64_t nq) {
     return best;
 }
 
-// workspace: xb (ntr x 64 bf16) | xaug (ntr x 16 bf16) | qb (nq x 64 bf16) | lists
+// workspace: xb (ntr x 64 bf16) | xaug (ntr x 16 bf16) | qb (nq x 64 bf16) | qaug (nq x 16 bf16) | lists
 // Operand buffers are padded to whole TMA boxes (a box may not exceed the
 // tensor): rows beyond nq / ntr hold garbage that is never reported (queries)
 // or masked to +inf (train columns) in the epilogue.
@@ -490,7 +502,8 @@ static inline int64_t pad_to(int64_t n, int64_t m) { return (n + m - 1) / m * m;
 size_t knn_tc_workspace(int64_t ntr, int64_t nq) {
     const int ns = knn_tc_nsplit(ntr, nq) > 0 ? knn_tc_nsplit(ntr, nq) : 0;
     const int64_t ntr_p = pad_to(ntr, KT_N), nq_p = pad_to(nq, KT_Q);
-    return (size_t)ntr_p * (KT_D + KT_AUG) * 2 + (size_t)nq_p * KT_D * 2 + 1024 + (size_t)nq * ns * KT_LPQ * KT_KMAX * 8 + 256 + 256;
+    return (size_t)ntr_p * (KT_D + KT_AUG) * 2 + (size_t)nq_p * (KT_D + KT_AUG) * 2 + 1024 +
+           (size_t)nq * ns * KT_LPQ * KT_KMAX * 8 + 256 + 256;
 }
 
 int knn_tc_run(const float* train, const float* query, const int* labels, int64_t ntr, int64_t nq, int k, int ncls,
@@ -500,7 +513,8 @@ int knn_tc_run(const float* train, const float* query, const int* labels, int64_
     __nv_bfloat16* xb = (__nv_bfloat16*)w;
     __nv_bfloat16* xaug = xb + (size_t)ntr_p * KT_D;
     __nv_bfloat16* qb = xaug + (size_t)ntr_p * KT_AUG;
-    uint64_t* lists = (uint64_t*)(((uintptr_t)(qb + (size_t)nq_p * KT_D) + 1023) & ~(uintptr_t)1023);
+    __nv_bfloat16* qaug = qb + (size_t)nq_p * KT_D;
+    uint64_t* lists = (uint64_t*)(((uintptr_t)(qaug + (size_t)nq_p * KT_AUG) + 1023) & ~(uintptr_t)1023);
     const int nsplit = knn_tc_nsplit(ntr, nq);
     if (nsplit < 0) {                                   // train set too long for the packed keys: SIMT
         cudaError_t e = cudaMemsetAsync(flag, 0x04, 1, st);
@@ -510,12 +524,14 @@ int knn_tc_run(const float* train, const float* query, const int* labels, int64_
     unsigned* maxn = (unsigned*)(lists + (size_t)nq * nsplit * KT_LPQ * KT_KMAX);
     cudaMemsetAsync(maxn, 0, 2 * sizeof(unsigned), st);
     const int pgrid = 4 * sm_count();
-    k_knn_prep<<<(unsigned)imin64(pgrid, (ntr + 15) / 16), 256, 0, st>>>(train, ntr, -2.f, xb, xaug, tnorm, flag, maxn);
-    k_knn_prep<<<(unsigned)imin64(pgrid, (nq + 15) / 16), 256, 0, st>>>(query, nq, 1.f, qb, nullptr, qnorm, flag, maxn + 1);
+    k_knn_prep<<<(unsigned)imin64(pgrid, (ntr + 15) / 16), 256, 0, st>>>(train, ntr, -2.f, false, xb, xaug, tnorm, flag, maxn);
+    k_knn_prep<<<(unsigned)imin64(pgrid, (nq + 15) / 16), 256, 0, st>>>(query, nq, 1.f, true, qb, qaug, qnorm, flag, maxn + 1);
     PMX_CHECK_LAUNCH("knn_prep");
-    CUtensorMap tmq, tmx, tmxa;
+    CUtensorMap tmq, tmqa, tmx, tmxa;
     if (!make_tmap_2d(&tmq, qb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)nq_p, KT_D, KT_Q, KT_D,
                       CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap_2d(&tmqa, qaug, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)nq_p, KT_AUG, KT_Q, KT_AUG,
+                      CU_TENSOR_MAP_SWIZZLE_32B) ||
         !make_tmap_2d(&tmx, xb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)ntr_p, KT_D, KT_N, KT_D,
                       CU_TENSOR_MAP_SWIZZLE_128B) ||
         !make_tmap_2d(&tmxa, xaug, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)ntr_p, KT_AUG, KT_N, KT_AUG,
@@ -528,7 +544,7 @@ int knn_tc_run(const float* train, const float* query, const int* labels, int64_
     cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = nitems < sm_count() ? nitems : sm_count();
     k_knn_bound<<<1, 32, 0, st>>>(maxn, flag);
-    k_knn_tc<<<grid, KT_THREADS, smem, st>>>(tmq, tmx, tmxa, ntr, nq, k, nsplit, lists, qnorm, flag);
+    k_knn_tc<<<grid, KT_THREADS, smem, st>>>(tmq, tmqa, tmx, tmxa, ntr, nq, k, nsplit, lists, flag);
     PMX_CHECK_LAUNCH("knn_tc");
     k_knn_merge<<<(unsigned)((nq + 127) / 128), 128, 0, st>>>(lists, nsplit * KT_LPQ, labels, nq, k, ncls, out_label,
                                                               out_idx, flag);

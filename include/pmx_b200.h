@@ -215,6 +215,12 @@ PMX_API int pmx_loop(const pmx_program* body, int64_t n, uint64_t* err, void* st
 PMX_API int pmx_seq_loop(const pmx_program* f, double* state, double* scratch,
                  int64_t m, int64_t steps, uint64_t* err, void* stream);
 
+/* The same with the initial state read from `init` (left unchanged) and the
+ * result in `state`: the copy of a caller's sequence into the iteration
+ * buffers is fused into step 0.       (seqLoop's input is an immutable value) */
+PMX_API int pmx_seq_loop_from(const pmx_program* f, const double* init, double* state, double* scratch,
+                      int64_t m, int64_t steps, uint64_t* err, void* stream);
+
 /* offsets[0]=0, offsets[i+1] = offsets[i] + lengths[i]  (int64).  Used to
  * flatten an irregular sequence: flatten is then the values buffer itself.
  *                                     replaces FlattenE interp.py:161-166 */

@@ -103,6 +103,7 @@ _SIGS = {
     "pmx_map_rows_fold": (C.c_int, [C.POINTER(Program), C.POINTER(Program), _P, C.c_int32, _P, C.c_int64, _P, _P,
                                     C.c_int32, _P, _P]),
     "pmx_seq_loop": (C.c_int, [C.POINTER(Program), _P, _P, C.c_int64, C.c_int64, _P, _P]),
+    "pmx_seq_loop_from": (C.c_int, [C.POINTER(Program), _P, _P, _P, C.c_int64, C.c_int64, _P, _P]),
     "pmx_scan_lengths": (C.c_int, [_P, _P, C.c_int64, _P]),
     "pmx_row_offsets": (C.c_int, [_P, C.c_int64, C.c_int64, _P]),
     "pmx_rk4_sweep_f64": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_double, _P, _P]),

@@ -33,7 +33,7 @@ int jit_map2(const pmx_program* f, const void* x, int xt, const void* y, int yt,
 int jit_loop(const pmx_program* body, int64_t n, uint64_t* err, cudaStream_t st);
 int jit_reduce_generic(const pmx_program* f, const pmx_program* op, const void* x, int xt, int64_t n,
                        const void* init_host, int acc_dtype, void* out, void* ws, cudaStream_t st, uint64_t* err);
-int jit_seq_loop(const pmx_program* f, double* a, double* b, int64_t m, int64_t steps, unsigned* bar,
+int jit_seq_loop(const pmx_program* f, const double* src, double* a, double* b, int64_t m, int64_t steps, unsigned* bar,
                  uint64_t* err, cudaStream_t st);
 int jit_map_reduce(const pmx_program* f, int okind, const void* x, int xt, int64_t n,
                    const void* init_host, void* out, void* y, int yt, void* ws, cudaStream_t st,

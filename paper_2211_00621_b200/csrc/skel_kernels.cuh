@@ -656,7 +656,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
 
 template <class F>
 __global__ void __launch_bounds__(256)
-k_seq_loop_jit(const F f, double* a, double* b, int64_t m, int64_t steps, unsigned* bar, uint64_t* err) {
+k_seq_loop_jit(const F f, const double* src, double* a, double* b, int64_t m, int64_t steps, unsigned* bar,
+               uint64_t* err) {
     F fl = f;
     fl.T[0].offset = 0;
     fl.T[0].shape[0] = m;
@@ -664,9 +665,9 @@ k_seq_loop_jit(const F f, double* a, double* b, int64_t m, int64_t steps, unsign
     fl.T[0].dtype = PMX_F64;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t = 0; t < steps; ++t) {
-        double* cur = (t & 1) ? b : a;
+        const double* cur = t == 0 ? src : ((t & 1) ? b : a);   // step 0 reads the caller's state
         double* nxt = (t & 1) ? a : b;
-        fl.T[0].data = cur;
+        fl.T[0].data = const_cast<double*>(cur);
         for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
             const int64_t x[1] = {__double_as_longlong(__ldcg(cur + j))}, jj[1] = {j}, tt[1] = {t};
             int64_t o[1];

@@ -341,14 +341,14 @@ __global__ void k_loop_vm(const __grid_constant__ pmx_program P, int64_t n, uint
 
 // Persistent seqLoop: `steps` iterations of a parallel map over the state,
 // one grid-wide barrier per step (cooperative launch).
-__global__ void k_seq_loop(pmx_program P, double* a, double* b, int64_t m, int64_t steps,
+__global__ void k_seq_loop(pmx_program P, const double* src, double* a, double* b, int64_t m, int64_t steps,
                            uint64_t* err) {
     cg::grid_group grid = cg::this_grid();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t = 0; t < steps; ++t) {
-        double* cur = (t & 1) ? b : a;
+        const double* cur = t == 0 ? src : ((t & 1) ? b : a);   // step 0 reads the caller's state
         double* nxt = (t & 1) ? a : b;
-        P.arrays[0].data = cur;   // previous state visible to GET through arrays[0]
+        P.arrays[0].data = const_cast<double*>(cur);   // previous state visible to GET through arrays[0]
         P.arrays[0].offset = 0;
         P.arrays[0].shape[0] = m;
         P.arrays[0].rank = 1;
@@ -700,17 +700,24 @@ int pmx_loop(const pmx_program* body, int64_t n, uint64_t* err, void* stream) {
     return 0;
 }
 
-int pmx_seq_loop(const pmx_program* f, double* state, double* scratch, int64_t m, int64_t steps,
-                 uint64_t* err, void* stream) {
-    PMX_REQUIRE(f && state && scratch, "pmx_seq_loop: null argument");
+int pmx_seq_loop_from(const pmx_program* f, const double* init, double* state, double* scratch, int64_t m,
+                      int64_t steps, uint64_t* err, void* stream) {
+    PMX_REQUIRE(f && init && state && scratch, "pmx_seq_loop: null argument");
     PMX_REQUIRE(f->n_arrays >= 1, "pmx_seq_loop: program must reserve arrays[0] for the state");
-    if (m <= 0 || steps <= 0) return 0;
+    if (m <= 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (steps <= 0) {
+        if (init != state) {
+            cudaError_t e = cudaMemcpyAsync(state, init, (size_t)m * sizeof(double), cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) { set_last_error("seq_loop: %s", cudaGetErrorString(e)); return -2; }
+        }
+        return 0;
+    }
     // run-time specialised persistent kernel (jit.cu); its grid-barrier word is
     // the 8-byte slot after the m scratch values (scratch holds m + 8 doubles)
     {
         unsigned* bar = reinterpret_cast<unsigned*>(scratch + m);
-        int jr = jit_seq_loop(f, state, scratch, m, steps, bar, err, st);
+        int jr = jit_seq_loop(f, init, state, scratch, m, steps, bar, err, st);
         if (jr < 0) return jr;
         if (jr == 0) {
             if (steps & 1) {
@@ -726,7 +733,7 @@ int pmx_seq_loop(const pmx_program* f, double* state, double* scratch, int64_t m
     if (per_sm < 1) per_sm = 1;
     int grid = grid_for(m, 256, per_sm);
     pmx_program P = *f;
-    void* args[] = {&P, &state, &scratch, &m, &steps, &err};
+    void* args[] = {&P, &init, &state, &scratch, &m, &steps, &err};
     cudaError_t e = cudaLaunchCooperativeKernel((void*)k_seq_loop, grid, 256, args, 0, st);
     if (e != cudaSuccess) { set_last_error("seq_loop: %s", cudaGetErrorString(e)); return -2; }
     if (steps & 1) {   // result landed in scratch: copy back so `state` holds it
@@ -734,6 +741,11 @@ int pmx_seq_loop(const pmx_program* f, double* state, double* scratch, int64_t m
         PMX_CHECK_LAUNCH("seq_loop copy");
     }
     return 0;
+}
+
+int pmx_seq_loop(const pmx_program* f, double* state, double* scratch, int64_t m, int64_t steps,
+                 uint64_t* err, void* stream) {
+    return pmx_seq_loop_from(f, state, state, scratch, m, steps, err, stream);
 }
 
 int pmx_row_offsets(int64_t* offsets, int64_t nrows, int64_t row_len, void* stream) {

@@ -575,13 +575,17 @@ def seq_loop(n: int, f, state, ctx: Optional[Ctx] = None, span: Span = NO_SPAN) 
     the captured placeholder `PREV` (see lam.get)."""
     ctx = ctx or default_ctx()
     s = _materialize(_as_seq(state, "seqLoop", span))
-    from .lambdas import lam
-    a = map_tensor(lam("x", "x"), s.data, _lib.PMX_F64, span)        # fresh fp64 state (one pmx_map)
-    b = torch.empty(a.numel() + 8, dtype=torch.float64, device=a.device)   # + grid-barrier word
+    if s.dtype_code == _lib.PMX_F64:
+        init = s.data.reshape(-1)                                      # read by step 0, left unchanged
+    else:
+        from .lambdas import lam
+        init = map_tensor(lam("x", "x"), s.data, _lib.PMX_F64, span)  # Float state in fp64 (one pmx_map)
+    a = torch.empty(init.numel(), dtype=torch.float64, device=init.device)
+    b = torch.empty(init.numel() + 8, dtype=torch.float64, device=init.device)   # + grid-barrier word
     prog = _compile(f, ["float", "int", "int"], span, state_array=PREV)
     err = ctx.new_err(span)
-    rc = _lib.load().pmx_seq_loop(C.byref(prog.program), a.data_ptr(), b.data_ptr(), a.numel(), int(n),
-                                  err.data_ptr(), ctx.stream_ptr())
+    rc = _lib.load().pmx_seq_loop_from(C.byref(prog.program), init.data_ptr(), a.data_ptr(), b.data_ptr(),
+                                       a.numel(), int(n), err.data_ptr(), ctx.stream_ptr())
     _lib.check(rc, "seq_loop")
     ctx.launches += 1
     return DeviceSeq(a, s.shape, _lib.PMX_F64)

@@ -4,6 +4,7 @@ goes through the C ABI (libpmxb200.so)."""
 import math
 
 import numpy as np
+import torch
 import pytest
 
 import oracle as O
@@ -295,6 +296,30 @@ def test_seq_loop_persistent_iteration():
     for _ in range(50):
         ref = 0.5 * (ref + np.roll(ref, -1))
     assert np.allclose(got, ref, rtol=1e-14)
+
+
+@pytest.mark.parametrize("steps", [0, 1, 2, 7])
+@pytest.mark.parametrize("m", [1000, 1 << 16])
+def test_seq_loop_leaves_input_and_counts_steps(steps, m):
+    # the initial state is an immutable value: step 0 reads it (pmx_seq_loop_from)
+    # and the caller's device sequence is unchanged afterwards; odd step counts
+    # land in the right buffer; both the interpreter (small m) and the
+    # specialised kernel (large m) paths
+    from paper_2211_00621_b200.runtime import seq_to_device
+    s0 = np.arange(m, dtype=np.float64) % 97
+    step = lam("x", "j", "t", addf(mulf(0.5, addf("x", get(PREV, modi(addi("j", 1), m)))), 1.0))
+
+    def body(s):
+        dev = seq_to_device(s) if not hasattr(s, "data") else s
+        before = dev.data.clone()
+        out = seq_loop(steps, step, dev)
+        assert torch.equal(dev.data, before)
+        return out
+    got = accelerate(body, s0)
+    ref = s0.copy()
+    for _ in range(steps):
+        ref = 0.5 * (ref + np.roll(ref, -1)) + 1.0
+    assert np.allclose(got, ref, rtol=1e-13)
 
 
 def test_map_rows_fold_irregular_and_regular(jit_mode):

@@ -547,8 +547,12 @@ def bench_knn(args, dist, peaks, pcie) -> dict:
                         "peak_source": "MEASURED_PEAKS.json bf16 dense (burst)",
                         "algorithmic_flops_per_query": 2 * d * ntr,
                         "tmem_read_bytes": 4.0 * ntr * nq,
-                        "note": "tcgen05 bf16 UMMA (exact for the integer data) with ||x||^2 folded into an "
-                                "augmentation k-step; each candidate distance leaves TMEM once (4 B)"},
+                        "tmem_read_probe_B_per_clk_per_SM": 451,
+                        "note": "tcgen05 bf16 UMMA (exact for the integer data) with ||x||^2 + ||q||^2 + 2^23 folded "
+                                "into an augmentation k-step; candidates leave TMEM as packed u16 distances "
+                                "(tcgen05.ld .pack::16b). Not TMEM-bound (profiles/tmem_probe.json: 451 B/clk/SM "
+                                "with 16 warps); shared-memory operand traffic (~780 clk/tile vs 640 of UMMA) and "
+                                "the two-buffer epilogue coupling bound it (DESIGN.md section 3)"},
            "kernels_per_step": 3}
     if not args.no_parity:
         O = _oracle()

@@ -279,17 +279,23 @@ def ir_eval(e, env: dict):
         return out
     if isinstance(e, L.Field):
         return ir_eval(e.rec, env)[e.label]
-    if isinstance(e, L.Iterate):             # linear recursion, base case upward
+    if isinstance(e, L.Iterate):             # k-term recursion, base cases upward
         lo, hi = ir_eval(e.lo, env), ir_eval(e.hi, env)
-        if hi - lo > L.ITERATE_LIMIT or hi - lo < -1:
+        k = 1 + len(e.more)
+        if hi - lo > L.ITERATE_LIMIT or hi - lo < -k:
             raise OracleError("maximum recursion depth exceeded")
-        acc = ir_eval(e.init, env)
+        names = [e.acc] + [n for n, _ in e.more]
+        inits = [e.init] + [x for _, x in e.more]
+        # accs[j] = f(lo - 1 - j); a base case is evaluated only when hi reaches it
+        accs = [ir_eval(x, env) if hi >= lo - 1 - j else 0 for j, x in enumerate(inits)]
+        if hi < lo:
+            return accs[lo - 1 - hi]
         for m in range(lo, hi + 1):
             env2 = dict(env)
             env2[e.var] = m
-            env2[e.acc] = acc
-            acc = ir_eval(e.body, env2)
-        return acc
+            env2.update(zip(names, accs))
+            accs = [ir_eval(e.body, env2)] + accs[:-1]
+        return accs[0]
     raise OracleError(f"ir_eval: unsupported node {type(e).__name__}")
 
 

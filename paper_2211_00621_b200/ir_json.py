@@ -55,7 +55,8 @@ def dump(lam: L.Lam) -> dict:
         if isinstance(e, L.Field):
             return ["Field", go(e.rec), e.label]
         if isinstance(e, L.Iterate):
-            return ["Iterate", e.var, go(e.lo), go(e.hi), e.acc, go(e.init), go(e.body)]
+            return ["Iterate", e.var, go(e.lo), go(e.hi), e.acc, go(e.init), go(e.body),
+                    [[n, go(x)] for n, x in e.more]]
         raise TypeError(type(e).__name__)
 
     return {"params": lam.params, "body": go(lam.body), "arrays": arrays}
@@ -94,7 +95,8 @@ def load(d: dict, make_array) -> L.Lam:
         if k == "Field":
             return L.Field(go(x[1]), x[2])
         if k == "Iterate":
-            return L.Iterate(x[1], go(x[2]), go(x[3]), x[4], go(x[5]), go(x[6]))
+            more = tuple((n, go(v)) for n, v in x[7]) if len(x) > 7 else ()
+            return L.Iterate(x[1], go(x[2]), go(x[3]), x[4], go(x[5]), go(x[6]), more)
         raise ValueError(k)
 
     return L.Lam(d["params"], go(d["body"])), arrays

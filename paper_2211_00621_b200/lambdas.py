@@ -129,13 +129,21 @@ class Iterate(Expr):
     The device form of a linear recursion f p = match p with c then base
     else E[f (p - 1)]: evaluated from the base case up, E applied with
     p = c+1 .. p (the reference evaluates the same expressions innermost
-    call first)."""
+    call first).
+
+    `more` generalises it to a k-term recurrence f p = E[f (p-1), .., f (p-k)]
+    with base cases at c .. c+k-1 (lo = c+k): acc holds f(m-1) and
+    more[i] = (name, init) holds f(m-2-i), initialised to f(lo-2-i).  A base
+    value is evaluated only when hi reaches its level (the reference only
+    evaluates the cases it recurses into); for hi in [lo-k, lo-1] the value is
+    that base case, below lo-k the recursion never reaches a base case."""
     var: str
     lo: Expr
     hi: Expr
     acc: str
     init: Expr
     body: Expr
+    more: tuple = ()
 
 
 @dataclass(eq=False)
@@ -516,6 +524,7 @@ def _compile(e: Expr, env: dict, g: _Gen) -> tuple[int, str, bool]:
         g.emit("NEVER")
         return g.const(0, "int"), "never", False
     if isinstance(e, Iterate):
+        k = 1 + len(e.more)
         lo, lt, lown = _compile(e.lo, env, g)
         hi, ht, hown = _compile(e.hi, env, g)
         if not (_int_like(lt) and _int_like(ht)):
@@ -527,8 +536,8 @@ def _compile(e: Expr, env: dict, g: _Gen) -> tuple[int, str, bool]:
             g.release(lo)
         if hown:
             g.release(hi)
-        # depth bound: -1 <= hi - lo <= ITERATE_LIMIT. hi < lo - 1 never reaches
-        # the base case (the reference recurses until its stack overflows); the
+        # depth bound: -k <= hi - lo <= ITERATE_LIMIT. hi < lo - k never reaches
+        # a base case (the reference recurses until its stack overflows); the
         # upper bound stands in for that stack (the reference overflows first)
         span, big = g.reg(), g.reg()
         g.emit("SUBI", span, h, m)
@@ -536,17 +545,42 @@ def _compile(e: Expr, env: dict, g: _Gen) -> tuple[int, str, bool]:
         ok = g.emit("JZ", 0, big)
         g.emit("FAIL", 0, 0, _lib_E_RECURSION)
         g.patch(ok, len(g.insns))
-        g.emit("LTI", big, span, g.const(-1, "int"))
+        g.emit("LTI", big, span, g.const(-k, "int"))
         ok = g.emit("JZ", 0, big)
         g.emit("FAIL", 0, 0, _lib_E_RECURSION)
         g.patch(ok, len(g.insns))
-        g.release(span)
         g.release(big)
-        a0, at, aown = _compile(e.init, env, g)
-        acc = g.reg()
-        g.emit("MOV", acc, a0)
-        if aown:
-            g.release(a0)
+        if k == 1:
+            g.release(span)
+        names = [e.acc] + [n for n, _ in e.more]
+        inits = [e.init] + [x for _, x in e.more]
+        accs = []
+        at = None
+        for j, (nm, x) in enumerate(zip(names, inits)):
+            # acc j holds f(lo - 1 - j): evaluated only when hi >= lo - 1 - j
+            acc = g.reg()
+            skip = None
+            if k > 1:
+                c = g.reg()
+                g.emit("GEQI", c, span, g.const(-1 - j, "int"))
+                skip = g.emit("JZ", 0, c)
+                g.release(c)
+            a0, t0, aown = _compile(x, env, g)
+            if at is None:
+                at = t0
+            elif t0 not in (at, "never") and at != "never":
+                raise CompileError("recursion base cases differ in type")
+            elif at == "never":
+                at = t0
+            g.emit("MOV", acc, a0)
+            if aown:
+                g.release(a0)
+            if skip is not None:
+                done = g.emit("JMP")
+                g.patch(skip, len(g.insns))
+                g.emit("MOV", acc, g.const(0, "int"))
+                g.patch(done, len(g.insns))
+            accs.append(acc)
         top = len(g.insns)
         c = g.reg()
         g.emit("LEQI", c, m, h)
@@ -554,11 +588,14 @@ def _compile(e: Expr, env: dict, g: _Gen) -> tuple[int, str, bool]:
         g.release(c)
         env2 = dict(env)
         env2[e.var] = (m, "int")
-        env2[e.acc] = (acc, at)
+        for nm, acc in zip(names, accs):
+            env2[nm] = (acc, at)
         b, bt, bown = _compile(e.body, env2, g)
-        if bt != at:
+        if bt != at and not (at == "never" or bt == "never"):
             raise CompileError("recursion step changes the result type")
-        g.emit("MOV", acc, b)
+        for j in range(k - 1, 0, -1):                  # shift: f(m-1-j) <- f(m-j)
+            g.emit("MOV", accs[j], accs[j - 1])
+        g.emit("MOV", accs[0], b)
         if bown:
             g.release(b)
         g.emit("ADDI", m, m, g.const(1, "int"))
@@ -567,7 +604,20 @@ def _compile(e: Expr, env: dict, g: _Gen) -> tuple[int, str, bool]:
         g.patch(jz, len(g.insns))
         g.release(m)
         g.release(h)
-        return acc, at, True
+        if k > 1:
+            # no step ran (hi < lo): the value is the base case f(hi) = acc[lo-1-hi]
+            res = g.reg()
+            g.emit("MOV", res, accs[0])
+            for j in range(1, k):
+                c = g.reg()
+                g.emit("EQI", c, span, g.const(-1 - j, "int"))
+                g.emit("SELECT", res, c, accs[j], res)
+                g.release(c)
+            g.release(span)
+            for acc in accs:
+                g.release(acc)
+            return res, at, True
+        return accs[0], at, True
     raise CompileError(f"cannot compile {type(e).__name__} for the device")
 
 

@@ -155,6 +155,8 @@ class _Translator:
 
     def apply_closure(self, clo, args, depth):
         rec = self.linear_recursion(clo, args, depth)
+        if rec is None:
+            rec = self.kterm_recursion(clo, args, depth)
         if rec is not None:
             return rec
         scope = {"__env__": clo.env}
@@ -255,12 +257,137 @@ class _Translator:
         step_scope = dict(scope)
         step_scope[pj] = L.Var(mvar)
         prev = getattr(self, "_rec_hole", None)
-        self._rec_hole = (call, accvar)
+        self._rec_hole = {id(call): accvar}
         try:
             step = self.as_expr(self.expr(m.els, step_scope, depth + 1))
         finally:
             self._rec_hole = prev
         out = L.Iterate(mvar, L.Const(c + 1, "int"), hi, accvar, init, step)
+        for n, a in reversed(binds):
+            out = L.LetE(n, a, out)
+        return out
+
+    def kterm_recursion(self, clo, args, depth):
+        """f p.. = match pj with c0 then B0 else match pj with c1 then B1 ...
+        else E[f p.. (subi pj d1), f p.. (subi pj d2), ..] with the base cases
+        c .. c+k-1 consecutive and 1 <= d <= k, d = 1 among them (so the
+        reference's top-down evaluation visits every level, e.g. fib) ->
+        Iterate from the base cases up with k accumulators (f(m-1) .. f(m-k)).
+        The calls must be strict: not under a match or a lambda of E, so the
+        bottom-up loop evaluates exactly the levels the reference does (once
+        each instead of exponentially often).  None if f is not of this form."""
+        S, R = self.S, self.R
+        params, body = self._peel(clo)
+        if len(params) != len(args) or not isinstance(body, S.Match):
+            return None
+        pj = None
+        bases = {}
+        e = body
+        while isinstance(e, S.Match):
+            if not (isinstance(e.scrut, S.Var) and e.scrut.name in params and isinstance(e.pat, S.PConst)
+                    and isinstance(e.pat.const, S.CInt)):
+                return None
+            if pj is None:
+                pj = e.scrut.name
+            elif e.scrut.name != pj:
+                return None
+            cv = int(e.pat.const.value)
+            if cv in bases:
+                return None
+            bases[cv] = e.thn
+            e = e.els
+        E = e
+        k = len(bases)
+        c = min(bases)
+        if k < 2 or sorted(bases) != list(range(c, c + k)):
+            return None
+
+        def resolves_to_self(name):
+            if name in params:
+                return None
+            try:
+                v = clo.env.lookup(name)
+            except AssertionError:
+                return None
+            if not isinstance(v, R.Closure):
+                return None
+            dps, dbody = self._peel(v)
+            return dps if dbody is body else None
+
+        if any(self._mentions_self(b, resolves_to_self) for b in bases.values()):
+            return None
+        calls = []
+
+        def walk(x):                                  # strict positions only
+            if isinstance(x, (S.Lam, S.Match)):
+                return not self._mentions_self(x, resolves_to_self)
+            if isinstance(x, S.App):
+                head, a = x, []
+                while isinstance(head, S.App):
+                    a.append(head.arg)
+                    head = head.fn
+                a.reverse()
+                if isinstance(head, S.Var):
+                    dps = resolves_to_self(head.name)
+                    if dps is not None:
+                        calls.append((x, dps, a))
+                        return all(not self._mentions_self(y, resolves_to_self) for y in a)
+                return walk(head) and all(walk(y) for y in a)
+            if isinstance(x, S.Let):
+                return walk(x.value) and walk(x.body)
+            if isinstance(x, S.Var):
+                return resolves_to_self(x.name) is None
+            return True
+
+        if not walk(E) or not calls:
+            return None
+        offsets = {}
+        for call, dps, cargs in calls:
+            if len(cargs) != len(dps):
+                return None
+            d = None
+            for q, a in zip(dps, cargs):
+                if q == pj:                           # subi pj d
+                    if not (isinstance(a, S.App) and isinstance(a.fn, S.App) and isinstance(a.fn.fn, S.ConstE)
+                            and isinstance(a.fn.fn.const, S.CBuiltin) and a.fn.fn.const.name == "subi"
+                            and isinstance(a.fn.arg, S.Var) and a.fn.arg.name == pj
+                            and isinstance(a.arg, S.ConstE) and isinstance(a.arg.const, S.CInt)):
+                        return None
+                    d = int(a.arg.const.value)
+                elif not (isinstance(a, S.Var) and a.name == q):
+                    return None
+            if d is None or not 1 <= d <= k:
+                return None
+            offsets[id(call)] = d
+        if 1 not in offsets.values():
+            return None
+        scope = {"__env__": clo.env}
+        binds = []
+        for prm, a in zip(params, args):
+            if isinstance(a, (_Fn, _Captured, L.Var)):
+                scope[prm] = a
+            else:
+                nm = self.fresh(prm.text)
+                scope[prm] = L.Var(nm)
+                binds.append((nm, a))
+        hi = self.as_expr(scope[pj])
+        mvar = self.fresh("rec_m")
+        accs = [self.fresh("rec_acc") for _ in range(k)]        # accs[j] = f(m - 1 - j)
+        inits = []
+        for j in range(k):
+            bs = dict(scope)
+            bs[pj] = L.Const(c + k - 1 - j, "int")
+            inits.append(self.as_expr(self.expr(bases[c + k - 1 - j], bs, depth + 1)))
+        step_scope = dict(scope)
+        step_scope[pj] = L.Var(mvar)
+        prev = getattr(self, "_rec_hole", None)
+        self._rec_hole = {cid: accs[d - 1] for cid, d in offsets.items()}
+        try:
+            step = self.as_expr(self.expr(E, step_scope, depth + 1))
+        finally:
+            self._rec_hole = prev
+        out = L.Iterate(mvar, L.Const(c + k, "int"), hi, accs[0], inits[0], step,
+                        tuple(zip(accs[1:], inits[1:])))
         for n, a in reversed(binds):
             out = L.LetE(n, a, out)
         return out
@@ -330,8 +457,8 @@ class _Translator:
     def expr(self, e, scope, depth):
         S = self.S
         hole = getattr(self, "_rec_hole", None)
-        if hole is not None and e is hole[0]:         # the recursive call: the loop's accumulator
-            return L.Var(hole[1])
+        if hole is not None and id(e) in hole:        # a recursive call: one of the loop's accumulators
+            return L.Var(hole[id(e)])
         if isinstance(e, S.Var):
             return self.lookup(e.name, scope)
         if isinstance(e, S.ConstE):

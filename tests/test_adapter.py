@@ -166,10 +166,29 @@ RECURSIVE = [
     ("let_in_step", "recursive let g = lam n. match n with 0 then 2 else let t = g (subi n 1) in "
                     "modi (addi (muli t t) n) 1000003 in "
                     "let r = accelerate (map g [0, 4, 50]) in print (int2string (reduce addi 0 r))", True),
-    # two recursive calls: not linear, stays unsupported on the device
+    # k-term recurrences -> device loop with k accumulators (kterm_recursion)
     ("fib", "recursive let fib = lam n. match n with 0 then 0 else match n with 1 then 1 else "
             "addi (fib (subi n 1)) (fib (subi n 2)) in "
-            "let r = accelerate (map fib [3, 7]) in print (int2string (reduce addi 0 r))", False),
+            "let r = accelerate (map fib [3, 7]) in print (int2string (reduce addi 0 r))", True),
+    ("fib_bases_only", "recursive let fib = lam n. match n with 0 then 0 else match n with 1 then 1 else "
+                       "addi (fib (subi n 1)) (fib (subi n 2)) in "
+                       "let r = accelerate (map fib [0, 1, 2, 15]) in print (int2string (reduce addi 0 r))", True),
+    ("trib_bases_reordered", "recursive let t = lam n. match n with 3 then 1 else match n with 1 then 0 else "
+                             "match n with 2 then 0 else addi (t (subi n 3)) (addi (t (subi n 1)) (t (subi n 2))) in "
+                             "let r = accelerate (map t [1, 2, 3, 4, 10, 13]) in "
+                             "print (int2string (reduce addi 0 r))", True),
+    ("kterm_float_let", "recursive let g = lam x. lam n. match n with 0 then x else match n with 1 then 1.0 else "
+                        "let a = g x (subi n 1) in let b = g x (subi n 2) in addf (mulf 0.5 a) (mulf x b) in "
+                        "let r = accelerate (map (lam n. g 0.25 n) [0, 1, 2, 9, 14]) in "
+                        "print (float2string (reduce addf 0.0 r))", True),
+    # recursive calls under a match of the step: the reference may skip levels, not lowered
+    ("kterm_lazy_call", "recursive let f = lam n. match n with 0 then 1 else match n with 1 then 2 else "
+                        "match modi n 2 with 0 then f (subi n 1) else addi (f (subi n 1)) (f (subi n 2)) in "
+                        "let r = accelerate (map f [5]) in print (int2string (reduce addi 0 r))", False),
+    # no f (n-1) call: the reference visits every other level only, not lowered
+    ("kterm_stride_two", "recursive let f = lam n. match n with 0 then 1 else match n with 1 then 1 else "
+                         "muli 3 (f (subi n 2)) in "
+                         "let r = accelerate (map f [6, 7]) in print (int2string (reduce addi 0 r))", False),
 ]
 
 
@@ -187,6 +206,21 @@ def test_linear_recursion_matches_reference(name, src, supported):
     finally:
         un()
     assert got == want
+
+
+def test_kterm_recursion_below_the_base_cases_is_an_error():
+    """fib n for n < 0 recurses forever in the reference; the device loop
+    reports the recursion error instead of returning a base case."""
+    pmx, interp = _pmx()
+    src = ("recursive let fib = lam n. match n with 0 then 0 else match n with 1 then 1 else "
+           "addi (fib (subi n 1)) (fib (subi n 2)) in "
+           "let r = accelerate (map fib [3, -1]) in print (int2string (reduce addi 0 r))")
+    un = install_checker(interp)
+    try:
+        with pytest.raises(pmx.Diagnostics, match="maximum recursion depth exceeded"):
+            pmx.run_source(src, mode="accel", workers=2, capture_output=True)
+    finally:
+        un()
 
 
 def test_recursion_that_never_reaches_the_base_case_is_an_error():

@@ -106,3 +106,41 @@ def test_check_determinism_warns_like_the_reference(pmx_installed, capsys):
     pmx.run_source(src, mode="accel", workers=4, check_determinism=True, capture_output=True)
     err = capsys.readouterr().err
     assert "warning: reduce result depends on the evaluation order" in err
+
+
+KTERM = [
+    ("recursive let fib = lam n. match n with 0 then 0 else match n with 1 then 1 else "
+     "addi (fib (subi n 1)) (fib (subi n 2)) in "
+     "let r = accelerate (map fib [0, 1, 2, 3, 7, 15]) in print (int2string (reduce addi 0 r))"),
+    ("recursive let t = lam n. match n with 3 then 1 else match n with 1 then 0 else "
+     "match n with 2 then 0 else addi (t (subi n 3)) (addi (t (subi n 1)) (t (subi n 2))) in "
+     "let r = accelerate (map t [1, 2, 3, 4, 10, 13]) in print (int2string (reduce addi 0 r))"),
+    ("recursive let g = lam x. lam n. match n with 0 then x else match n with 1 then 1.0 else "
+     "let a = g x (subi n 1) in let b = g x (subi n 2) in addf (mulf 0.5 a) (mulf x b) in "
+     "let r = accelerate (map (lam n. g 0.25 n) [0, 1, 2, 9, 14]) in print (float2string (reduce addf 0.0 r))"),
+]
+
+
+@pytest.mark.parametrize("src", KTERM, ids=["fib", "tribonacci", "kterm_float"])
+def test_kterm_recursion_through_the_dropin(pmx_installed, src):
+    # non-linear (k-term) recursion runs as a device loop with k accumulators;
+    # the reference's own debug mode is the expected output
+    pmx, _ = pmx_installed
+    want = pmx.run_source(src, mode="debug", capture_output=True).stdout
+    got = pmx.run_source(src, mode="accel", workers=4, capture_output=True).stdout
+    assert tokens_match(got, want, float_rel=1e-12), (got, want)
+
+
+def test_kterm_recursion_at_specialised_kernel_size(pmx_installed):
+    # 70,000 elements: the map runs in the run-time specialised kernel (above
+    # the interpreter threshold); expected value from the closed iteration
+    pmx, _ = pmx_installed
+    src = ("recursive let fib = lam n. match n with 0 then 0 else match n with 1 then 1 else "
+           "addi (fib (subi n 1)) (fib (subi n 2)) in "
+           "let r = accelerate (map fib (create 70000 (lam i. modi i 45))) in print (int2string (reduce addi 0 r))")
+    f = [0, 1]
+    while len(f) < 45:
+        f.append(f[-1] + f[-2])
+    want = sum(f[i % 45] for i in range(70000))
+    got = pmx.run_source(src, mode="accel", workers=4, capture_output=True).stdout
+    assert int(got) == want

@@ -474,13 +474,17 @@ def bench_rk4(args, dist, peaks, pcie) -> dict:
     pinned = torch.from_numpy(host_ps).pin_memory()
     e2e_ms, _ = host_time(lambda: P.accelerate(lambda p, s: CS.rk4_sweep(p, s, m, synth.RK4_H), pinned,
                                                 synth.RK4_INIT), 3, 1, dist)
-    # FP64 pipe work per parameter-step, from the ncu capture of k_rk4 (thread-level
-    # DADD + DMUL + DFMA executed / 10^7 param-steps); the reference as written
-    # does ~104 add/mul + 12 sin/cos per step
+    # Algorithmic FP64 work per parameter-step: the program as written (~104
+    # add/mul and a full sin/cos per stage, 12 per step) costs 272 FP64 pipe
+    # instructions per param-step (ncu thread-level DADD + DMUL + DFMA of k_rk4
+    # with a full fdlibm-class sin/cos per stage, profiles/rk4_fp64.json). The
+    # default kernel does less trig work (angle addition), so this
+    # fixed figure over its time is the algorithmic rate, not its own count
     pp = pipe_peaks()
     prof = _rk4_profile()
     fp64_peak = pp.get("fp64_add_ops_per_s", 63.0 * 148 * 1.965e9)
-    roof = {"bound": "fp64 pipe, latency-limited: N = 10^4 threads = 68 per SM (2 warps per SM sub-partition)",
+    roof = {"bound": "fp64 pipe, latency-limited: N = 10^4 threads = 68 per SM (2 warps per SM sub-partition); "
+                     "work = the as-written evaluation's 272 FP64 pipe instructions per param-step",
             "unit": "fp64 pipe instr/s", "peak": fp64_peak,
             "peak_source": "tools/peaks.cu (profiles/pipe_peaks.json): 63 DADD/DFMA per clk per SM"}
     if prof:

@@ -65,7 +65,27 @@ __device__ __forceinline__ SinCos sincos_cw(double x) {
 // per parameter set splitting the two reductions, with shuffles, 0.63 ms;
 // Estrin instead of Horner 0.63 ms; 32/64/128-thread CTAs all equal — the
 // time is one warp's dependent chain, ~1200 cycles per RK4 step.)
-enum { RK4_LIBM = 0, RK4_FAST = 1 };
+enum { RK4_LIBM = 0, RK4_FAST = 1, RK4_ADD = 2 };
+
+// sin and cos of a small increment d (|d| <= 1/8: the next terms are below
+// 2^-60 relative), Taylor series to d^13 / d^12 in Horner form on d^2.
+__device__ __forceinline__ SinCos sincos_small(double d) {
+    const double z = d * d;
+    const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, -1.6059043836821614599e-10, 2.5052108385441718775e-08),
+                                            -2.7557319223985890653e-06), 1.9841269841269841270e-04),
+                                 -8.3333333333333333333e-03), 1.6666666666666666667e-01);
+    const double pc = fma(z, fma(z, fma(z, fma(z, fma(z, 2.0876756987868098979e-09, -2.7557319223985890653e-07),
+                                            2.4801587301587301587e-05), -1.3888888888888888889e-03),
+                                 4.1666666666666666667e-02), -0.5);
+    return SinCos{fma(-d * z, ps, d), fma(z, pc, 1.0)};
+}
+
+// sin/cos(x0 + d) from sin/cos(x0) and of the small increment d:
+// angle addition, two fused products each (the result is within ~2 ulp, like
+// a direct evaluation; parity is checked at 1e-9 relative)
+__device__ __forceinline__ SinCos sincos_add(const SinCos& b, const SinCos& e) {
+    return SinCos{fma(b.s, e.c, b.c * e.s), fma(b.c, e.c, -(b.s * e.s))};
+}
 
 template <int MODE>
 __device__ __forceinline__ void trig(const St& s, double& sa, double& sp, double& cp, bool& bad) {
@@ -94,6 +114,16 @@ __device__ __forceinline__ St deriv(double p, const St& s, bool& bad) {
     return d;
 }
 
+// deriv with the trig values supplied (RK4_ADD computes them by angle addition)
+__device__ __forceinline__ St deriv_t(double p, const St& s, double sa, double sp, double cp) {
+    St d;
+    d.x0 = s.x1;
+    d.x1 = S_(M_(p, M_(sp, cp)), A_(M_(0.2, s.x1), M_(0.3, sa)));
+    d.x2 = s.x3;
+    d.x3 = S_(-M_(9.81, sp), A_(M_(0.1, s.x3), M_(p, M_(s.x1, cp))));
+    return d;
+}
+
 // axpy s c d = map2 (lam x. lam dx. addf x (mulf c dx)) s d   (rk4.pmx:23-25)
 __device__ __forceinline__ St axpy(const St& s, double c, const St& d) {
     return St{A_(s.x0, M_(c, d.x0)), A_(s.x1, M_(c, d.x1)), A_(s.x2, M_(c, d.x2)), A_(s.x3, M_(c, d.x3))};
@@ -104,9 +134,58 @@ __device__ __forceinline__ double comb(double s, double h6, double k1, double k2
     return A_(s, M_(h6, A_(k1, A_(M_(2.0, k2), A_(M_(2.0, k3), k4)))));
 }
 
+// step p s with RK4_ADD trig: one full sin/cos of the step's two angles; the
+// stage arguments s_i = s + c k (rk4.pmx:27-29) are the base angles plus a
+// small increment (h/2 or h times a velocity), whose sin/cos is a short series
+// available as soon as the increment is — so the three later stages no
+// longer wait on a full argument reduction and polynomial.
+// (A, B): sin/cos of the step's two angles s.x0 and s.x2
+__device__ __forceinline__ St step_add_t(double p, const St& s, const SinCos& A, const SinCos& B, double h,
+                                         double h2, double h6, bool& bad) {
+    auto stage_trig = [&](const St& si, double& sa, double& sp, double& cp) {
+        const double da = __dsub_rn(si.x0, s.x0), dp = __dsub_rn(si.x2, s.x2);
+        bad |= !(fabs(da) <= 0.125 && fabs(dp) <= 0.125);
+        const SinCos a = sincos_add(A, sincos_small(da)), b = sincos_add(B, sincos_small(dp));
+        sa = a.s; sp = b.s; cp = b.c;
+    };
+    const St k1 = deriv_t(p, s, A.s, B.s, B.c);
+    double sa, sp, cp;
+    const St s2 = axpy(s, h2, k1);
+    stage_trig(s2, sa, sp, cp);
+    const St k2 = deriv_t(p, s2, sa, sp, cp);
+    const St s3 = axpy(s, h2, k2);
+    stage_trig(s3, sa, sp, cp);
+    const St k3 = deriv_t(p, s3, sa, sp, cp);
+    const St s4 = axpy(s, h, k3);
+    stage_trig(s4, sa, sp, cp);
+    const St k4 = deriv_t(p, s4, sa, sp, cp);
+    return St{comb(s.x0, h6, k1.x0, k2.x0, k3.x0, k4.x0), comb(s.x1, h6, k1.x1, k2.x1, k3.x1, k4.x1),
+              comb(s.x2, h6, k1.x2, k2.x2, k3.x2, k4.x2), comb(s.x3, h6, k1.x3, k2.x3, k3.x3, k4.x3)};
+}
+
+__device__ __forceinline__ St step_add(double p, const St& s, double h, double h2, double h6, bool& bad) {
+    const SinCos A = sincos_cw(s.x0), B = sincos_cw(s.x2);
+    bad |= !(fabs(s.x0) <= 262144.0 && fabs(s.x2) <= 262144.0);
+    return step_add_t(p, s, A, B, h, h2, h6, bad);
+}
+
+// two steps with one full sin/cos: the second step's angles are the first
+// step's plus a small increment, so its base sin/cos come by angle addition
+// too (a full reduction every other step bounds the accumulated rounding)
+__device__ __forceinline__ St step2_add(double p, const St& s, double h, double h2, double h6, bool& bad) {
+    const SinCos A = sincos_cw(s.x0), B = sincos_cw(s.x2);
+    bad |= !(fabs(s.x0) <= 262144.0 && fabs(s.x2) <= 262144.0);
+    const St s1 = step_add_t(p, s, A, B, h, h2, h6, bad);
+    const double da = __dsub_rn(s1.x0, s.x0), dp = __dsub_rn(s1.x2, s.x2);
+    bad |= !(fabs(da) <= 0.125 && fabs(dp) <= 0.125);
+    const SinCos A1 = sincos_add(A, sincos_small(da)), B1 = sincos_add(B, sincos_small(dp));
+    return step_add_t(p, s1, A1, B1, h, h2, h6, bad);
+}
+
 // step p s (rk4.pmx:26-37)
 template <int MODE>
 __device__ __forceinline__ St step(double p, const St& s, double h, double h2, double h6, bool& bad) {
+    if (MODE == RK4_ADD) return step_add(p, s, h, h2, h6, bad);
     const St k1 = deriv<MODE>(p, s, bad);
     const St k2 = deriv<MODE>(p, axpy(s, h2, k1), bad);
     const St k3 = deriv<MODE>(p, axpy(s, h2, k2), bad);
@@ -137,8 +216,13 @@ k_rk4(const double* __restrict__ ps, int64_t n, const double* __restrict__ init4
         // schedules the explicit pair best).
         for (; m + 1 < steps; m += 2) {
             bool bad = false;
-            const St s1 = step<MODE>(p, s, h, h2, h6, bad);
-            const St s2 = step<MODE>(p, s1, h, h2, h6, bad);
+            St s2;
+            if (MODE == RK4_ADD) {
+                s2 = step2_add(p, s, h, h2, h6, bad);
+            } else {
+                const St s1 = step<MODE>(p, s, h, h2, h6, bad);
+                s2 = step<MODE>(p, s1, h, h2, h6, bad);
+            }
             if (bad) {
                 bool unused = false;
                 s = step<RK4_LIBM>(p, step<RK4_LIBM>(p, s, h, h2, h6, unused), h, h2, h6, unused);
@@ -169,9 +253,13 @@ k_rk4(const double* __restrict__ ps, int64_t n, const double* __restrict__ init4
 
 using namespace pmx;
 
-// PMX_RK4_MODE=0 selects CUDA's libm sin/sincos (A/B and tests); default FAST.
+// PMX_RK4_MODE=0 selects CUDA's libm sin/sincos, 1 the per-stage fast sin/cos
+// (A/B and tests); default 2 (one fast sin/cos per step + angle addition).
 static int rk4_mode() {
-    static const int v = [] { const char* e = getenv("PMX_RK4_MODE"); return e && e[0] == '0' ? 0 : 1; }();
+    static const int v = [] {
+        const char* e = getenv("PMX_RK4_MODE");
+        return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : 2;
+    }();
     return v;
 }
 
@@ -183,8 +271,10 @@ static void rk4_launch(const double* params, int64_t n, const double* init4, int
     const int64_t grid = (n + threads - 1) / threads;
     if (rk4_mode() == RK4_LIBM)
         k_rk4<TRACE, RK4_LIBM><<<(unsigned)grid, threads, 0, st>>>(params, n, init4, steps, h, out, comp, trace);
-    else
+    else if (rk4_mode() == RK4_FAST)
         k_rk4<TRACE, RK4_FAST><<<(unsigned)grid, threads, 0, st>>>(params, n, init4, steps, h, out, comp, trace);
+    else
+        k_rk4<TRACE, RK4_ADD><<<(unsigned)grid, threads, 0, st>>>(params, n, init4, steps, h, out, comp, trace);
 }
 
 extern "C" int pmx_rk4_sweep_f64(const double* params, int64_t n, const double* init4,

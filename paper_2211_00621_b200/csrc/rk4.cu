@@ -66,17 +66,20 @@ __device__ __forceinline__ SinCos sincos_cw(double x) {
 // Estrin instead of Horner 0.63 ms; 32/64/128-thread CTAs all equal — the
 // time is one warp's dependent chain, ~1200 cycles per RK4 step.)
 enum { RK4_LIBM = 0, RK4_FAST = 1, RK4_ADD = 2 };
+#ifndef RK4_ADD_BLOCK
+#define RK4_ADD_BLOCK 4      // steps per full sin/cos in RK4_ADD (one straight-line block)
+#endif
 
-// sin and cos of a small increment d (|d| <= 1/8: the next terms are below
-// 2^-60 relative), Taylor series to d^13 / d^12 in Horner form on d^2.
+// sin and cos of a small increment d (|d| <= 1/16, checked by the caller: the
+// omitted terms are below 2^-64 relative), Taylor series to d^9 / d^8 in
+// Estrin form on z = d^2 (dependent depth 4-5 instead of 7).
 __device__ __forceinline__ SinCos sincos_small(double d) {
-    const double z = d * d;
-    const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, -1.6059043836821614599e-10, 2.5052108385441718775e-08),
-                                            -2.7557319223985890653e-06), 1.9841269841269841270e-04),
-                                 -8.3333333333333333333e-03), 1.6666666666666666667e-01);
-    const double pc = fma(z, fma(z, fma(z, fma(z, fma(z, 2.0876756987868098979e-09, -2.7557319223985890653e-07),
-                                            2.4801587301587301587e-05), -1.3888888888888888889e-03),
-                                 4.1666666666666666667e-02), -0.5);
+    const double z = d * d, z2 = z * z;
+    const double ps = fma(z2, fma(z, -2.7557319223985890653e-06, 1.9841269841269841270e-04),
+                          fma(z, -8.3333333333333333333e-03, 1.6666666666666666667e-01));
+    const double pc = fma(z2 * z2, -2.7557319223985890653e-07,
+                          fma(z2, fma(z, 2.4801587301587301587e-05, -1.3888888888888888889e-03),
+                              fma(z, 4.1666666666666666667e-02, -0.5)));
     return SinCos{fma(-d * z, ps, d), fma(z, pc, 1.0)};
 }
 
@@ -136,7 +139,7 @@ __device__ __forceinline__ double comb(double s, double h6, double k1, double k2
 
 // step p s with RK4_ADD trig: one full sin/cos of the step's two angles; the
 // stage arguments s_i = s + c k (rk4.pmx:27-29) are the base angles plus a
-// small increment (h/2 or h times a velocity), whose sin/cos is a short series
+// small increment (h/2 or h times a velocity; at most 0.015 on the bench sweep), whose sin/cos is a short series
 // available as soon as the increment is — so the three later stages no
 // longer wait on a full argument reduction and polynomial.
 // (A, B): sin/cos of the step's two angles s.x0 and s.x2
@@ -144,7 +147,7 @@ __device__ __forceinline__ St step_add_t(double p, const St& s, const SinCos& A,
                                          double h2, double h6, bool& bad) {
     auto stage_trig = [&](const St& si, double& sa, double& sp, double& cp) {
         const double da = __dsub_rn(si.x0, s.x0), dp = __dsub_rn(si.x2, s.x2);
-        bad |= !(fabs(da) <= 0.125 && fabs(dp) <= 0.125);
+        bad |= !(fabs(da) <= 0.0625 && fabs(dp) <= 0.0625);
         const SinCos a = sincos_add(A, sincos_small(da)), b = sincos_add(B, sincos_small(dp));
         sa = a.s; sp = b.s; cp = b.c;
     };
@@ -172,14 +175,22 @@ __device__ __forceinline__ St step_add(double p, const St& s, double h, double h
 // two steps with one full sin/cos: the second step's angles are the first
 // step's plus a small increment, so its base sin/cos come by angle addition
 // too (a full reduction every other step bounds the accumulated rounding)
-__device__ __forceinline__ St step2_add(double p, const St& s, double h, double h2, double h6, bool& bad) {
-    const SinCos A = sincos_cw(s.x0), B = sincos_cw(s.x2);
+template <int NS>
+__device__ __forceinline__ St stepn_add(double p, St s, double h, double h2, double h6, bool& bad) {
+    SinCos A = sincos_cw(s.x0), B = sincos_cw(s.x2);
     bad |= !(fabs(s.x0) <= 262144.0 && fabs(s.x2) <= 262144.0);
-    const St s1 = step_add_t(p, s, A, B, h, h2, h6, bad);
-    const double da = __dsub_rn(s1.x0, s.x0), dp = __dsub_rn(s1.x2, s.x2);
-    bad |= !(fabs(da) <= 0.125 && fabs(dp) <= 0.125);
-    const SinCos A1 = sincos_add(A, sincos_small(da)), B1 = sincos_add(B, sincos_small(dp));
-    return step_add_t(p, s1, A1, B1, h, h2, h6, bad);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        const St s1 = step_add_t(p, s, A, B, h, h2, h6, bad);
+        if (i + 1 < NS) {
+            const double da = __dsub_rn(s1.x0, s.x0), dp = __dsub_rn(s1.x2, s.x2);
+            bad |= !(fabs(da) <= 0.0625 && fabs(dp) <= 0.0625);
+            A = sincos_add(A, sincos_small(da));
+            B = sincos_add(B, sincos_small(dp));
+        }
+        s = s1;
+    }
+    return s;
 }
 
 // step p s (rk4.pmx:26-37)
@@ -214,20 +225,22 @@ k_rk4(const double* __restrict__ ps, int64_t n, const double* __restrict__ init4
         // the fast reduction's range in either.  Measured 0.615 -> 0.532 ms; three
         // steps per block 0.624, a rolled 2- or 4-step loop 0.58 / 0.64 (ptxas
         // schedules the explicit pair best).
-        for (; m + 1 < steps; m += 2) {
+        constexpr int NB = MODE == RK4_ADD ? RK4_ADD_BLOCK : 2;
+        for (; m + NB - 1 < steps; m += NB) {
             bool bad = false;
-            St s2;
+            St sn;
             if (MODE == RK4_ADD) {
-                s2 = step2_add(p, s, h, h2, h6, bad);
+                sn = stepn_add<NB>(p, s, h, h2, h6, bad);
             } else {
                 const St s1 = step<MODE>(p, s, h, h2, h6, bad);
-                s2 = step<MODE>(p, s1, h, h2, h6, bad);
+                sn = step<MODE>(p, s1, h, h2, h6, bad);
             }
             if (bad) {
                 bool unused = false;
-                s = step<RK4_LIBM>(p, step<RK4_LIBM>(p, s, h, h2, h6, unused), h, h2, h6, unused);
+#pragma unroll 1
+                for (int i = 0; i < NB; ++i) s = step<RK4_LIBM>(p, s, h, h2, h6, unused);
             } else {
-                s = s2;
+                s = sn;
             }
         }
     }

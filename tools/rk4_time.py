@@ -26,6 +26,6 @@ for _ in range(10):
     b.synchronize()
     ts.append(a.elapsed_time(b))
 res = out.data.cpu().numpy()
-tag = os.environ.get("PMX_RK4_MODE", "1")
+tag = os.environ.get("PMX_RK4_MODE", "2")
 np.save(f"gpurun_out/rk4_out_{tag}.npy", res)
 print(json.dumps({"mode": tag, "ms_min": min(ts), "ms_med": sorted(ts)[5]}))

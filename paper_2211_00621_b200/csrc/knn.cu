@@ -59,7 +59,8 @@ k_knn(const float* __restrict__ train, const float* __restrict__ tnorm, const in
       int64_t ntr, const float* __restrict__ query, const float* __restrict__ qnorm, int64_t nq, int d,
       int k, int ncls, int* __restrict__ out_label, int* __restrict__ out_idx,
       const unsigned* __restrict__ run_if) {
-    if (run_if && *run_if == 0) return;     // the tensor-core path produced the answer
+    if (run_if && (*run_if & 7u) == 0) return;   // the tensor-core path produced the answer (flag bit 8:
+                                                   // its bf16 form instead of int8)
     extern __shared__ __align__(16) float sm[];
     float* QsT = sm;                                  // [d][QT]
     float* XsT = QsT + KNN_DMAX * KNN_QT;             // [d][TT]

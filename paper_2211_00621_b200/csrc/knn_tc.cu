@@ -65,16 +65,30 @@ constexpr int KT_KMAX = 8;
 constexpr int KT_EW = 16;                 // epilogue warps
 constexpr int KT_THREADS = 64 + 32 * KT_EW;
 constexpr int KT_LPQ = 2;                 // partial lists per query per item (column halves)
-constexpr uint32_t KT_A_BYTES = KT_Q * KT_D * 2;        // 32 KB
-constexpr uint32_t KT_AAUG_BYTES = KT_Q * KT_AUG * 2;   //  8 KB
-constexpr uint32_t KT_B_BYTES = KT_N * KT_D * 2;        // 16 KB
-constexpr uint32_t KT_BAUG_BYTES = KT_N * KT_AUG * 2;   //  4 KB
+// Operand formats of the tensor-core kernel.  Rows are K-major byte strings:
+// 64 coordinates (bf16: 128 B, SWIZZLE_128B; int8: 64 B, SWIZZLE_64B) and a
+// 32-byte augmentation row (SWIZZLE_32B).  Every UMMA consumes 32 bytes of K.
+//   BF16: kind::f16, fp32 accumulation, D = dist + 2^23 (low 16 bits = dist)
+//   I8:   kind::i8, int32 accumulation, D = dist (exact by construction)
+struct OpsBF16 {
+    static constexpr int ROWB = 128, KSTEPS = 4;
+    static constexpr uint32_t IDESC = tc::instr_desc(128, 128, 1);
+    static constexpr unsigned FLAG_RUN = 8;       // runs when only the int8 form is inexact
+};
+struct OpsI8 {
+    static constexpr int ROWB = 64, KSTEPS = 2;
+    // c_format S32 (2), a/b signed int8 (1), K-major, N >> 3, M >> 4
+    static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+    static constexpr unsigned FLAG_RUN = 0;
+};
+constexpr int KT_AUGB = 32;                       // augmentation row bytes (16 bf16 / 32 int8)
 
+template <class Ops>
 struct __align__(1024) KnnSmem {
-    __nv_bfloat16 A[KT_Q * KT_D];                       // 2 halves of 128 rows, SW128
-    __nv_bfloat16 B[KT_STAGES][KT_N * KT_D];            // SW128
-    __nv_bfloat16 Aaug[KT_Q * KT_AUG];                  // query augmentation rows (2 halves), SW32
-    __nv_bfloat16 Baug[KT_STAGES][KT_N * KT_AUG];       // SW32
+    uint8_t A[KT_Q * Ops::ROWB];                        // 2 halves of 128 query rows
+    uint8_t B[KT_STAGES][KT_N * Ops::ROWB];             // train rows per tile
+    uint8_t Aaug[KT_Q * KT_AUGB];                       // query augmentation rows (2 halves)
+    uint8_t Baug[KT_STAGES][KT_N * KT_AUGB];
     uint64_t full[KT_STAGES], empty[KT_STAGES];
     uint64_t a_full, a_empty;
     uint64_t tfull[2], tempty[2];
@@ -197,6 +211,7 @@ __global__ void k_knn_prep(const float* __restrict__ x, int64_t rows, float scal
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     bool inexact = false;
     float nmax = 0.f;
+    const bool write_ops = (*flag & 8u) != 0;   // bf16 operands only when the int8 form is inexact
     for (int64_t w = wid; w * 2 < rows; w += nw) {          // warp-uniform trip count
         const int64_t r = w * 2 + ((threadIdx.x >> 4) & 1);
         const bool valid = r < rows;
@@ -218,13 +233,13 @@ __global__ void k_knn_prep(const float* __restrict__ x, int64_t rows, float scal
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, 16);
         if (valid) {
-            reinterpret_cast<uint2*>(xb + r * 64)[sub] = packed;
+            if (sub == 0) inexact |= !(s >= 0.f && s < 65536.f && s == floorf(s));
+            if (write_ops) reinterpret_cast<uint2*>(xb + r * 64)[sub] = packed;
             nmax = fmaxf(nmax, s);
             if (sub == 0) norms[r] = s;
-            if (sub < 4) {
+            if (sub < 4 && write_ops) {
                 // hi, lo are exact in bf16 when s is an integer in [0, 2^16)
                 const float hi = floorf(s / 256.f), lo = s - 256.f * hi;
-                if (sub == 0) inexact |= !(s >= 0.f && s < 65536.f && s == floorf(s));
                 auto bf = [](float v) { return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v)); };
                 uint2 a = make_uint2(0u, 0u);
                 if (sub == 0) {
@@ -243,6 +258,50 @@ __global__ void k_knn_prep(const float* __restrict__ x, int64_t rows, float scal
     if ((threadIdx.x & 31) == 0) atomicMax(maxn, __float_as_uint(nmax));    // norms >= 0: bits order as values
 }
 
+// int8 operands (the default tensor-core form): train -2x, query q as signed
+// 8-bit integers, augmentation rows (32 bytes) train [a, b, 64, 1, 0...] and
+// query [64, 1, a, b, 0...] with ||v||^2 = 64 a + b, so the int32 accumulator
+// is exactly ||x||^2 - 2 q.x + ||q||^2.  flag |= 8 when a scaled coordinate is
+// not an integer in [-128, 127] or a norm not an integer below 8192 (the bf16
+// form then runs).
+__global__ void k_knn_prep8(const float* __restrict__ x, int64_t rows, float scale, bool is_query,
+                            int8_t* __restrict__ xb, int8_t* __restrict__ xaug, unsigned* __restrict__ flag) {
+    const int sub = threadIdx.x & 15;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    bool inexact = false;
+    for (int64_t w = wid; w * 2 < rows; w += nw) {
+        const int64_t r = w * 2 + ((threadIdx.x >> 4) & 1);
+        const bool valid = r < rows;
+        const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(x + r * 64) + sub)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float f[4] = {v.x, v.y, v.z, v.w};
+        uint32_t packed = 0;
+        float s = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float sv = scale * f[e];
+            inexact |= !(sv == rintf(sv) && sv >= -128.f && sv <= 127.f);
+            packed |= (uint32_t)(uint8_t)(int8_t)(int)fminf(fmaxf(sv, -128.f), 127.f) << (8 * e);
+            s = fmaf(f[e], f[e], s);
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, 16);
+        if (valid) {
+            reinterpret_cast<uint32_t*>(xb + r * 64)[sub] = packed;
+            if (sub < 2) {
+                const bool ok = s >= 0.f && s < 8192.f && s == floorf(s);
+                if (sub == 0) inexact |= !ok;
+                const uint32_t a = ok ? (uint32_t)(s / 64.f) : 0u, b = ok ? (uint32_t)s - 64u * a : 0u;
+                uint4 row = make_uint4(0u, 0u, 0u, 0u);
+                if (sub == 0) row.x = is_query ? (64u | (1u << 8) | (a << 16) | (b << 24)) : (a | (b << 8) | (64u << 16) | (1u << 24));
+                reinterpret_cast<uint4*>(xaug + r * KT_AUGB)[sub] = row;
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, inexact) && (threadIdx.x & 31) == 0) atomicOr(flag, 8u);
+}
+
 // The packed keys hold squared distances up to KT_DIST_MAX: with the largest
 // norms (sqrt(max ||x||^2) + sqrt(max ||q||^2))^2 bounds every distance; above
 // it the SIMT kernel answers (flag bit 2).
@@ -253,15 +312,18 @@ __global__ void k_knn_bound(const unsigned* __restrict__ maxn, unsigned* __restr
     }
 }
 
+template <class Ops>
 __global__ void __maxnreg__(96)
 k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmqa,
          const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmxa, int64_t ntr, int64_t nq,
          int k, int nsplit, uint64_t* __restrict__ lists, const unsigned* __restrict__ flag) {
-    if (*flag) return;                       // inexact data: the SIMT path answers
+    if (*flag != Ops::FLAG_RUN) return;      // the other format (or the SIMT kernel) answers
+    constexpr uint32_t A_BYTES = KT_Q * Ops::ROWB, AAUG_BYTES = KT_Q * KT_AUGB;
+    constexpr uint32_t B_BYTES = KT_N * Ops::ROWB, BAUG_BYTES = KT_N * KT_AUGB;
     extern __shared__ uint8_t smem_raw[];
     // 1 KiB-aligned by pointer arithmetic on the __shared__ array itself, so every
     // access through it stays in the shared space (STS/LDS, not generic ST/LD)
-    KnnSmem& S = *reinterpret_cast<KnnSmem*>(
+    KnnSmem<Ops>& S = *reinterpret_cast<KnnSmem<Ops>*>(
         smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nblk = (int)((nq + KT_Q - 1) / KT_Q);
@@ -301,12 +363,12 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                 const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
                 if (!first) { tc::mbar_wait(&S.a_empty, a_par); a_par ^= 1; }
                 first = false;
-                tc::mbar_arrive_expect_tx(&S.a_full, KT_A_BYTES + KT_AAUG_BYTES);
+                tc::mbar_arrive_expect_tx(&S.a_full, A_BYTES + AAUG_BYTES);
                 tc::tma_load_2d(S.A, &tmq, &S.a_full, 0, qb * KT_Q);
                 tc::tma_load_2d(S.Aaug, &tmqa, &S.a_full, 0, qb * KT_Q);
                 for (int t = t0; t < t1; ++t) {
                     tc::mbar_wait(&S.empty[stage], phase ^ 1);
-                    tc::mbar_arrive_expect_tx(&S.full[stage], KT_B_BYTES + KT_BAUG_BYTES);
+                    tc::mbar_arrive_expect_tx(&S.full[stage], B_BYTES + BAUG_BYTES);
                     tc::tma_load_2d(S.B[stage], &tmx, &S.full[stage], 0, t * KT_N);
                     tc::tma_load_2d(S.Baug[stage], &tmxa, &S.full[stage], 0, t * KT_N);
                     if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
@@ -316,11 +378,14 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
     } else if (warp == 1) {
         // ---- MMA issuer: the whole warp walks the pipeline (uniform registers),
         // one elected lane issues; descriptors advance in 16-byte units
-        constexpr uint32_t idesc = tc::instr_desc(KT_M, KT_N, 1);
+        constexpr uint32_t idesc = Ops::IDESC;
         int stage = 0; uint32_t phase = 0, a_par = 0;
         int b = 0; uint32_t acc_phase = 0;
-        const uint64_t a_desc = tc::sw128_kmajor_desc(tc::smem_u32(S.A));
-        const uint64_t b_desc0 = tc::sw128_kmajor_desc(tc::smem_u32(S.B[0]));
+        auto main_desc = [](const void* p) {
+            return Ops::ROWB == 128 ? tc::sw128_kmajor_desc(tc::smem_u32(p)) : tc::sw64_kmajor_desc(tc::smem_u32(p));
+        };
+        const uint64_t a_desc = main_desc(S.A);
+        const uint64_t b_desc0 = main_desc(S.B[0]);
         const uint64_t aaug_desc = tc::sw32_kmajor_desc(tc::smem_u32(S.Aaug));
         const uint64_t baug_desc0 = tc::sw32_kmajor_desc(tc::smem_u32(S.Baug[0]));
         for (int it = it_begin; it < it_end; ++it) {
@@ -332,17 +397,22 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                 tc::mbar_wait(&S.full[stage], phase);
                 tc::tc_fence_after();
                 if (tc::elect_one()) {
-                    const uint64_t bd = b_desc0 + (uint64_t)(stage * (KT_B_BYTES >> 4));
-                    const uint64_t bad = baug_desc0 + (uint64_t)(stage * (KT_BAUG_BYTES >> 4));
+                    const uint64_t bd = b_desc0 + (uint64_t)(stage * (B_BYTES >> 4));
+                    const uint64_t bad = baug_desc0 + (uint64_t)(stage * (BAUG_BYTES >> 4));
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const uint32_t d = tmem + (uint32_t)((b * 2 + h) * KT_N);
-                        const uint64_t ad = a_desc + (uint64_t)(h * ((KT_M * KT_D * 2) >> 4));
+                        const uint64_t ad = a_desc + (uint64_t)(h * ((KT_M * Ops::ROWB) >> 4));
+                        // K advances 32 bytes (2 descriptor units) per UMMA
 #pragma unroll
-                        for (int kk = 0; kk < KT_D / 16; ++kk)
-                            tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, kk > 0);
-                        // + ||x||^2 + ||q||^2 + 2^23 (the half's 128 query augmentation rows)
-                        tc::umma_f16(d, aaug_desc + (uint64_t)(h * ((KT_M * KT_AUG * 2) >> 4)), bad, idesc, 1);
+                        for (int kk = 0; kk < Ops::KSTEPS; ++kk) {
+                            if (Ops::ROWB == 128) tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, kk > 0);
+                            else tc::umma_i8(d, ad + 2 * kk, bd + 2 * kk, idesc, kk > 0);
+                        }
+                        // + ||x||^2 + ||q||^2 (+ 2^23 for the bf16 form)
+                        const uint64_t aad = aaug_desc + (uint64_t)(h * ((KT_M * KT_AUGB) >> 4));
+                        if (Ops::ROWB == 128) tc::umma_f16(d, aad, bad, idesc, 1);
+                        else tc::umma_i8(d, aad, bad, idesc, 1);
                     }
                     tc::umma_commit(&S.empty[stage]);
                     tc::umma_commit(&S.tfull[b]);
@@ -416,7 +486,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
 __global__ void k_knn_merge(const uint64_t* __restrict__ lists, int nlists, const int* __restrict__ labels,
                             int64_t nq, int k, int ncls, int* __restrict__ out_label, int* __restrict__ out_idx,
                             const unsigned* __restrict__ flag) {
-    if (*flag) return;
+    if (*flag & 7u) return;                  // the SIMT kernel answers
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
     const uint64_t* P = lists + q * nlists * KT_KMAX;
@@ -499,11 +569,26 @@ int knn_tc_nsplit(int64_t ntr, int64_t nq) {
 // or masked to +inf (train columns) in the epilogue.
 static inline int64_t pad_to(int64_t n, int64_t m) { return (n + m - 1) / m * m; }
 
+// workspace: bf16 operands (train 64 + 16 aug, query 64 + 16 aug per row) |
+// int8 operands (64 + 32 bytes per row each) | lists | maxn
 size_t knn_tc_workspace(int64_t ntr, int64_t nq) {
     const int ns = knn_tc_nsplit(ntr, nq) > 0 ? knn_tc_nsplit(ntr, nq) : 0;
     const int64_t ntr_p = pad_to(ntr, KT_N), nq_p = pad_to(nq, KT_Q);
-    return (size_t)ntr_p * (KT_D + KT_AUG) * 2 + (size_t)nq_p * (KT_D + KT_AUG) * 2 + 1024 +
+    return (size_t)(ntr_p + nq_p) * (KT_D + KT_AUG) * 2 + (size_t)(ntr_p + nq_p) * (64 + KT_AUGB) + 2048 +
            (size_t)nq * ns * KT_LPQ * KT_KMAX * 8 + 256 + 256;
+}
+
+template <class Ops>
+static int knn_tc_launch(const CUtensorMap& tmq, const CUtensorMap& tmqa, const CUtensorMap& tmx,
+                         const CUtensorMap& tmxa, int64_t ntr, int64_t nq, int k, int nsplit, uint64_t* lists,
+                         const unsigned* flag, cudaStream_t st) {
+    const int nitems = (int)((nq + KT_Q - 1) / KT_Q) * nsplit;
+    const size_t smem = sizeof(KnnSmem<Ops>) + 1024;
+    cudaFuncSetAttribute(k_knn_tc<Ops>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = nitems < sm_count() ? nitems : sm_count();
+    k_knn_tc<Ops><<<grid, KT_THREADS, smem, st>>>(tmq, tmqa, tmx, tmxa, ntr, nq, k, nsplit, lists, flag);
+    PMX_CHECK_LAUNCH("knn_tc");
+    return 0;
 }
 
 int knn_tc_run(const float* train, const float* query, const int* labels, int64_t ntr, int64_t nq, int k, int ncls,
@@ -514,7 +599,11 @@ int knn_tc_run(const float* train, const float* query, const int* labels, int64_
     __nv_bfloat16* xaug = xb + (size_t)ntr_p * KT_D;
     __nv_bfloat16* qb = xaug + (size_t)ntr_p * KT_AUG;
     __nv_bfloat16* qaug = qb + (size_t)nq_p * KT_D;
-    uint64_t* lists = (uint64_t*)(((uintptr_t)(qaug + (size_t)nq_p * KT_AUG) + 1023) & ~(uintptr_t)1023);
+    int8_t* xb8 = (int8_t*)(((uintptr_t)(qaug + (size_t)nq_p * KT_AUG) + 1023) & ~(uintptr_t)1023);
+    int8_t* xaug8 = xb8 + (size_t)ntr_p * 64;
+    int8_t* qb8 = xaug8 + (size_t)ntr_p * KT_AUGB;
+    int8_t* qaug8 = qb8 + (size_t)nq_p * 64;
+    uint64_t* lists = (uint64_t*)(((uintptr_t)(qaug8 + (size_t)nq_p * KT_AUGB) + 1023) & ~(uintptr_t)1023);
     const int nsplit = knn_tc_nsplit(ntr, nq);
     if (nsplit < 0) {                                   // train set too long for the packed keys: SIMT
         cudaError_t e = cudaMemsetAsync(flag, 0x04, 1, st);
@@ -524,28 +613,34 @@ int knn_tc_run(const float* train, const float* query, const int* labels, int64_
     unsigned* maxn = (unsigned*)(lists + (size_t)nq * nsplit * KT_LPQ * KT_KMAX);
     cudaMemsetAsync(maxn, 0, 2 * sizeof(unsigned), st);
     const int pgrid = 4 * sm_count();
-    k_knn_prep<<<(unsigned)imin64(pgrid, (ntr + 15) / 16), 256, 0, st>>>(train, ntr, -2.f, false, xb, xaug, tnorm, flag, maxn);
-    k_knn_prep<<<(unsigned)imin64(pgrid, (nq + 15) / 16), 256, 0, st>>>(query, nq, 1.f, true, qb, qaug, qnorm, flag, maxn + 1);
+    const unsigned gtr = (unsigned)imin64(pgrid, (ntr + 15) / 16), gq = (unsigned)imin64(pgrid, (nq + 15) / 16);
+    // int8 operands first (flag bit 8 when inexact); then norms, the bf16
+    // exactness bit and — only if the int8 form is inexact — the bf16 operands
+    k_knn_prep8<<<gtr, 256, 0, st>>>(train, ntr, -2.f, false, xb8, xaug8, flag);
+    k_knn_prep8<<<gq, 256, 0, st>>>(query, nq, 1.f, true, qb8, qaug8, flag);
+    k_knn_prep<<<gtr, 256, 0, st>>>(train, ntr, -2.f, false, xb, xaug, tnorm, flag, maxn);
+    k_knn_prep<<<gq, 256, 0, st>>>(query, nq, 1.f, true, qb, qaug, qnorm, flag, maxn + 1);
     PMX_CHECK_LAUNCH("knn_prep");
-    CUtensorMap tmq, tmqa, tmx, tmxa;
-    if (!make_tmap_2d(&tmq, qb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)nq_p, KT_D, KT_Q, KT_D,
-                      CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap_2d(&tmqa, qaug, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)nq_p, KT_AUG, KT_Q, KT_AUG,
-                      CU_TENSOR_MAP_SWIZZLE_32B) ||
-        !make_tmap_2d(&tmx, xb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)ntr_p, KT_D, KT_N, KT_D,
-                      CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_tmap_2d(&tmxa, xaug, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)ntr_p, KT_AUG, KT_N, KT_AUG,
-                      CU_TENSOR_MAP_SWIZZLE_32B)) {
+    CUtensorMap tmq, tmqa, tmx, tmxa, tmq8, tmqa8, tmx8, tmxa8;
+    const CUtensorMapDataType BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, U8 = CU_TENSOR_MAP_DATA_TYPE_UINT8;
+    if (!make_tmap_2d(&tmq, qb, BF, 2, (uint64_t)nq_p, KT_D, KT_Q, KT_D, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap_2d(&tmqa, qaug, BF, 2, (uint64_t)nq_p, KT_AUG, KT_Q, KT_AUG, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !make_tmap_2d(&tmx, xb, BF, 2, (uint64_t)ntr_p, KT_D, KT_N, KT_D, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap_2d(&tmxa, xaug, BF, 2, (uint64_t)ntr_p, KT_AUG, KT_N, KT_AUG, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !make_tmap_2d(&tmq8, qb8, U8, 1, (uint64_t)nq_p, 64, KT_Q, 64, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !make_tmap_2d(&tmqa8, qaug8, U8, 1, (uint64_t)nq_p, KT_AUGB, KT_Q, KT_AUGB, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !make_tmap_2d(&tmx8, xb8, U8, 1, (uint64_t)ntr_p, 64, KT_N, 64, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !make_tmap_2d(&tmxa8, xaug8, U8, 1, (uint64_t)ntr_p, KT_AUGB, KT_N, KT_AUGB, CU_TENSOR_MAP_SWIZZLE_32B)) {
         set_last_error("knn: cuTensorMapEncodeTiled unavailable or failed");
         return -2;
     }
-    const int nitems = (int)((nq + KT_Q - 1) / KT_Q) * nsplit;
-    const size_t smem = sizeof(KnnSmem) + 1024;
-    cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int grid = nitems < sm_count() ? nitems : sm_count();
     k_knn_bound<<<1, 32, 0, st>>>(maxn, flag);
-    k_knn_tc<<<grid, KT_THREADS, smem, st>>>(tmq, tmqa, tmx, tmxa, ntr, nq, k, nsplit, lists, flag);
-    PMX_CHECK_LAUNCH("knn_tc");
+    // exactly one of these does the work (flag == 0: int8, flag == 8: bf16); the
+    // other returns at once, as both do when the SIMT kernel answers
+    int rc = knn_tc_launch<OpsI8>(tmq8, tmqa8, tmx8, tmxa8, ntr, nq, k, nsplit, lists, flag, st);
+    if (rc) return rc;
+    rc = knn_tc_launch<OpsBF16>(tmq, tmqa, tmx, tmxa, ntr, nq, k, nsplit, lists, flag, st);
+    if (rc) return rc;
     k_knn_merge<<<(unsigned)((nq + 127) / 128), 128, 0, st>>>(lists, nsplit * KT_LPQ, labels, nq, k, ncls, out_label,
                                                               out_idx, flag);
     PMX_CHECK_LAUNCH("knn_merge");

@@ -126,6 +126,14 @@ __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a_desc, uint
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
         :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
 }
+// kind::i8 (signed / unsigned 8-bit integers, int32 accumulate)
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
 // Arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
@@ -199,6 +207,18 @@ __device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t smem_addr) {
     d |= (uint64_t)(1024 >> 4) << 32;                     // SBO = 1024 B    [32,46)
     d |= (uint64_t)1 << 46;                               // version = 1 (sm_100) [46,48)
     d |= (uint64_t)2 << 61;                               // layout: SWIZZLE_128B [61,64)
+    return d;
+}
+
+// Same for the SWIZZLE_64B K-major layout (rows of 64 bytes, 8-row atoms of
+// 512 bytes; 16-byte chunk c of row r sits at c ^ ((r >> 1) & 3)).
+__device__ __forceinline__ uint64_t sw64_kmajor_desc(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;                      // SBO = 512 B
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;                               // layout: SWIZZLE_64B
     return d;
 }
 

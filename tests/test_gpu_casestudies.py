@@ -226,6 +226,22 @@ def test_knn_integer_ranges_exact(lo, hi, ntr, nq, k):
     assert np.array_equal(lab, olab)
 
 
+def test_knn_half_integer_queries_take_the_bf16_form():
+    # queries with eight coordinates at +-0.5 (the rest integers): not int8-exact,
+    # bf16-exact with integer norms -> the bf16 tensor-core kernel (flag 8); exact
+    rng = np.random.default_rng(11)
+    X = rng.integers(-6, 7, size=(3000, 64)).astype(np.float32)
+    Q = rng.integers(-6, 7, size=(200, 64)).astype(np.float32)
+    for r in range(200):
+        cols = rng.choice(64, size=8, replace=False)
+        Q[r, cols] = rng.choice([-0.5, 0.5], size=8)
+    L = synth.knn_labels(3000, 10)
+    lab, idx = accelerate(lambda x, l, q: knn_classify(x, l, q, 8, 10, return_indices=True), X, L, Q)
+    olab, oidx = O.knn(X, L, Q, 8, 10)
+    assert np.array_equal(idx, oidx)
+    assert np.array_equal(lab, olab)
+
+
 def test_knn_continuous_data_is_tie_tolerant():
     rng = np.random.default_rng(3)
     X = rng.random((3000, 64), dtype=np.float32)

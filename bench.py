@@ -546,17 +546,21 @@ def bench_knn(args, dist, peaks, pcie) -> dict:
            "pair_dims_per_s": float(ntr) * NQ * d / (ms * 1e-3),
            "e2e": _e2e("queries/s", NQ, e2e_ms / 2, pX.numel() * 4 + pQ.numel() * 4 + pL.numel() * 4, nq * 4,
                        pcie, "accelerate(knn_classify) with pinned host train / labels / queries"),
-           "roofline": {"bound": "tensor", "unit": "TFLOP/s", "achieved": achieved,
-                        "peak": peaks["bf16_tflops"], "frac": achieved / peaks["bf16_tflops"],
-                        "peak_source": "MEASURED_PEAKS.json bf16 dense (burst)",
+           "roofline": {"bound": "tensor (int8)", "unit": "TOP/s", "achieved": achieved,
+                        "peak": 2.0 * peaks["bf16_tflops"], "frac": achieved / (2.0 * peaks["bf16_tflops"]),
+                        "peak_source": "int8 dense = 2 x the measured bf16 dense peak (MEASURED_PEAKS.json, burst; "
+                                       "B200_PROFILING.md: int8/fp8 dense = 2 x bf16); the UMMA issue probe "
+                                       "reaches 4.53 POP/s kind::i8 (profiles/umma_rate.json)",
+                        "frac_vs_bf16_peak": achieved / peaks["bf16_tflops"],
                         "algorithmic_flops_per_query": 2 * d * ntr,
                         "tmem_read_bytes": 4.0 * ntr * nq,
                         "tmem_read_probe_B_per_clk_per_SM": 451,
-                        "note": "tcgen05 bf16 UMMA (exact for the integer data) with ||x||^2 + ||q||^2 + 2^23 folded "
-                                "into an augmentation k-step; candidates leave TMEM as packed u16 distances "
-                                "(tcgen05.ld .pack::16b). Not TMEM-bound (profiles/tmem_probe.json: 451 B/clk/SM "
-                                "with 16 warps); shared-memory operand traffic (~780 clk/tile vs 640 of UMMA) and "
-                                "the two-buffer epilogue coupling bound it (DESIGN.md section 3)"},
+                        "note": "tcgen05 kind::i8 UMMA on int8 operands (the integer data are exact in int8; bf16 "
+                                "form for data that are not) with exact int32 accumulation of ||x||^2 - 2q.x + "
+                                "||q||^2 (norms folded into an augmentation k-step); candidates leave TMEM as "
+                                "packed u16 distances (tcgen05.ld .pack::16b). Not TMEM-bound (451 B/clk/SM with "
+                                "16 warps); shared-memory operand traffic and the two-buffer epilogue coupling "
+                                "bound it (DESIGN.md section 3)"},
            "kernels_per_step": 3}
     if not args.no_parity:
         O = _oracle()

@@ -12,7 +12,7 @@ using namespace pmx;
 
 constexpr int ITER = 4096;
 
-template <int N>
+template <int N, bool I8>
 __global__ void __launch_bounds__(128, 1) k_umma(int* sink) {
     extern __shared__ uint8_t raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -29,13 +29,18 @@ __global__ void __launch_bounds__(128, 1) k_umma(int* sink) {
     tc::tc_fence_after();
     const uint32_t tmem = tbase;
     if (threadIdx.x == 0) {
-        constexpr uint32_t idesc = tc::instr_desc(128, N, 0);
+        // kind::f16 (fp16, K = 16 per UMMA) or kind::i8 (signed int8, int32 accumulate, K = 32)
+        constexpr uint32_t idesc = I8 ? ((2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24))
+                                      : tc::instr_desc(128, N, 0);
         const uint64_t bd = tc::sw128_kmajor_desc(tc::smem_u32(B));
         for (int it = 0; it < ITER; ++it) {
             const uint64_t ad = tc::sw128_kmajor_desc(tc::smem_u32(A + (it & 3) * 16384));
             const uint32_t d = tmem + (uint32_t)((it & 1) * 256);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, kk != 0);
+            for (int kk = 0; kk < 4; ++kk) {
+                if (I8) tc::umma_i8(d, ad + 2 * kk, bd + 2 * kk, idesc, kk != 0);
+                else tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, kk != 0);
+            }
         }
         tc::umma_commit(&done);
     }
@@ -47,13 +52,13 @@ __global__ void __launch_bounds__(128, 1) k_umma(int* sink) {
     if (threadIdx.x == 0 && tmem == 12345u) *sink = 1;
 }
 
-template <int N>
+template <int N, bool I8 = false>
 static void run(int sms) {
     const size_t smem = 4 * 16384 + N * 128 + 2048;
-    cudaFuncSetAttribute(k_umma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_umma<N, I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int* sink;
     cudaMalloc(&sink, 4);
-    k_umma<N><<<sms, 128, smem>>>(sink);
+    k_umma<N, I8><<<sms, 128, smem>>>(sink);
     cudaDeviceSynchronize();
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -61,16 +66,17 @@ static void run(int sms) {
     float best = 1e30f;
     for (int r = 0; r < 5; ++r) {
         cudaEventRecord(a);
-        k_umma<N><<<sms, 128, smem>>>(sink);
+        k_umma<N, I8><<<sms, 128, smem>>>(sink);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         if (ms < best) best = ms;
     }
-    const double flop = (double)sms * ITER * 4 * 2.0 * 128 * N * 16;
-    printf("{\"M\": 128, \"N\": %d, \"K\": 16, \"tflops\": %.1f, \"ms\": %.4f, \"err\": \"%s\"}\n", N,
-           flop / (best * 1e-3) / 1e12, best, cudaGetErrorString(cudaGetLastError()));
+    const int K = I8 ? 32 : 16;
+    const double flop = (double)sms * ITER * 4 * 2.0 * 128 * N * K;
+    printf("{\"kind\": \"%s\", \"M\": 128, \"N\": %d, \"K\": %d, \"tflops\": %.1f, \"ms\": %.4f, \"err\": \"%s\"}\n",
+           I8 ? "i8" : "f16", N, K, flop / (best * 1e-3) / 1e12, best, cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
@@ -80,5 +86,7 @@ int main() {
     run<64>(sms);
     run<128>(sms);
     run<256>(sms);
+    run<128, true>(sms);
+    run<256, true>(sms);
     return 0;
 }

@@ -331,7 +331,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
 #pragma unroll
                         for (int s = 0; s < 16; ++s) d[s] = pv;
                     }
-                    float csum[16], v[16];
+                    float v[16];
 #pragma unroll
                     for (int s = 0; s < 16; ++s) v[s] = d[s] * ev[s] * ic[s];
                     // Precision guard: an entry >= 32 of u' (which sums to 2^10 c_t <= 2^11)
@@ -348,28 +348,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                             if (v[s] >= 32.f && s0 + sb + s < nsig) atomicAdd(&events[s0 + sb + s], 1);
                     }
 #pragma unroll
-                    for (int s = 0; s < 16; s += 2) {
-                        const __half2 u2 = __floats2half2_rn(v[s], v[s + 1]);
-                        uh[ch * 8 + s / 2] = u2;
-                        const float2 f2 = __half22float2(u2);
-                        csum[s] = f2.x;
-                        csum[s + 1] = f2.y;
-                    }
-                    // sums over the warp's 32 states: fold the lane halves, then transpose-reduce
-                    // 16 values over 16 lanes (lane l < 16 ends with signal sb + l)
-#pragma unroll
-                    for (int s = 0; s < 16; ++s) csum[s] += __shfl_xor_sync(0xffffffffu, csum[s], 16);
-#pragma unroll
-                    for (int w = 8; w > 0; w >>= 1) {
-                        const bool upper = (lane & w) != 0;
-#pragma unroll
-                        for (int s = 0; s < w; ++s) {
-                            const float send = upper ? csum[s] : csum[s + w];
-                            const float keep = upper ? csum[s + w] : csum[s];
-                            csum[s] = keep + __shfl_xor_sync(0xffffffffu, send, w);
-                        }
-                    }
-                    if (lane < 16) Sm.wsum[q][sb + lane] += csum[0];   // M block 0, then 1 (same warp)
+                    for (int s = 0; s < 16; s += 2) uh[ch * 8 + s / 2] = __floats2half2_rn(v[s], v[s + 1]);
                 }
                 if (lead) stamp(t, 4 * mb);
                 // (2) store, once both pairs' MMAs of t consumed my rows of u_{t-1} (gdone):
@@ -411,8 +390,38 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                     hq_bulk_commit();
                 }
                 if (lead) stamp(t, 3 + 2 * mb);
+                // (3) per-signal sums of the stored (fp16-rounded) values over the warp's 32
+                // states — after the stores, off the path to the next step's first UMMAs
+                // (the sums are folded one step late): fold the lane halves, then
+                // transpose-reduce 16 values over 16 lanes (lane l < 16 ends with signal
+                // sb + l)
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch) {
+                    const int sb = hq * 32 + ch * 16;
+                    float csum[16];
+#pragma unroll
+                    for (int s = 0; s < 16; s += 2) {
+                        const float2 f2 = __half22float2(uh[ch * 8 + s / 2]);
+                        csum[s] = f2.x;
+                        csum[s + 1] = f2.y;
+                    }
+#pragma unroll
+                    for (int s = 0; s < 16; ++s) csum[s] += __shfl_xor_sync(0xffffffffu, csum[s], 16);
+#pragma unroll
+                    for (int w = 8; w > 0; w >>= 1) {
+                        const bool upper = (lane & w) != 0;
+#pragma unroll
+                        for (int s = 0; s < w; ++s) {
+                            const float send = upper ? csum[s] : csum[s + w];
+                            const float keep = upper ? csum[s + w] : csum[s];
+                            csum[s] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+                        }
+                    }
+                    if (lane < 16) Sm.wsum[q][sb + lane] += csum[0];   // M block 0, then 1 (same warp)
+                }
             }
             if (lead && t + 1 < T) hq_bulk_wait_read();      // my rows free for the next step
+            asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");   // every warp's sums in wsum
             // my partial of every signal -> all four CTAs (own slot written locally)
             float part = 0.f;
             if (ew < 4) {

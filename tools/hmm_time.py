@@ -6,7 +6,8 @@ sys.path.insert(0, str(ROOT))
 import numpy as np, torch
 from paper_2211_00621_b200 import _lib, casestudies as CS, synth
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
-S, K, nsig = 1024, 8, 4096
+S, K = 1024, 8
+nsig = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
 A, E, pi = synth.hmm_model(S, K)
 dev = torch.device("cuda")
 Ad = torch.from_numpy(A.astype(np.float32)).to(dev)
@@ -20,5 +21,5 @@ f(); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); f(); e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
-print(f"tc={os.environ.get('PMX_HMM_TC','f16')} dbg={os.environ.get('PMX_HMM_DBG','0')} T={T}: {ms:.2f} ms "
+print(f"tc={os.environ.get('PMX_HMM_TC','f16')} dbg={os.environ.get('PMX_HMM_DBG','0')} nsig={nsig} T={T}: {ms:.2f} ms "
       f"-> {ms * 9999 / (T - 1):.1f} ms at T=10^4, {ms / (T - 1) * 1e3:.2f} us/step")

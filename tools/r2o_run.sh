@@ -1,0 +1,17 @@
+# r2o: evidence refresh after k-NN int8 and the HMM sums change: full GPU tests, smoke, bench
+# (ours + reference arm), launch list, ncu --set full of k-NN (int8, full config) and the HMM quad kernel
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+  --log-file gpurun_out/r2o_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-parity > gpurun_out/bench_ncu.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_knn -c 1 -o gpurun_out/r2o_prof_knn python tools/profile_cases.py knn_full > /dev/null 2>&1
+ncu -i gpurun_out/r2o_prof_knn.ncu-rep --page raw --csv > gpurun_out/r2o_knn_raw.csv 2>/dev/null
+ncu -i gpurun_out/r2o_prof_knn.ncu-rep --page source --csv > gpurun_out/r2o_knn_source.csv 2>/dev/null
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_hmm_fwd_quad -c 1 -o gpurun_out/r2o_prof_hmm python tools/profile_cases.py hmm > /dev/null 2>&1
+ncu -i gpurun_out/r2o_prof_hmm.ncu-rep --page raw --csv > gpurun_out/r2o_hmm_raw.csv 2>/dev/null
+ncu -i gpurun_out/r2o_prof_hmm.ncu-rep --page source --csv > gpurun_out/r2o_hmm_source.csv 2>/dev/null
+ls gpurun_out

@@ -277,6 +277,31 @@ def test_kmer_vs_oracle(kmer, nsig, T):
     assert np.allclose(got, want, rtol=LL_REL, atol=0)
 
 
+@pytest.mark.parametrize("nsig,T", [(1, 1), (3, 2), (75, 9), (149, 5), (200, 17)])
+def test_kmer8_cluster_signal_loop(nsig, T):
+    # k = 8 runs on CTA pairs (k_kmer_fwd_pair), one signal per pair at a time:
+    # fewer signals than pairs, one extra signal past a whole round (75, 149 with
+    # 74 pairs), several rounds, and T = 1 (no exchange step inside a signal)
+    E = synth.kmer_emission(8, 8)
+    obs = synth.hmm_obs(nsig, T, 8)
+    got = accelerate(lambda em, o: hmm_kmer_forward(8, 0.5, 0.125, em, o), E, obs)
+    want = O.kmer_forward_scaled(8, 0.5, 0.125, E, obs)
+    assert np.allclose(got, want, rtol=LL_REL, atol=0)
+
+
+def test_kmer8_cluster_peaked_emissions():
+    # emissions spanning ~9 decades (state-dependent), stay/step not summing to 1
+    S, K = 1 << 16, 8
+    j = np.arange(S)[:, None]
+    k = np.arange(K)[None, :]
+    E = np.exp(-((j * 7 + k * 5) % 23) * 0.9)
+    E /= E.sum(axis=1, keepdims=True)
+    obs = synth.hmm_obs(6, 40, K)
+    got = accelerate(lambda em, o: hmm_kmer_forward(8, 0.7, 0.05, em, o), E, obs)
+    want = O.kmer_forward_scaled(8, 0.7, 0.05, E, obs)
+    assert np.allclose(got, want, rtol=LL_REL, atol=0)
+
+
 # ---------------------------------------------------------- NN gradients
 def _nn_ref_data():
     n_in, n_out, n_pts = 16, 8, 32

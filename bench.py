@@ -657,20 +657,26 @@ def bench_kmer(args, dist, peaks, pcie) -> dict:
     pobs = torch.from_numpy(hobs).pin_memory()
     e2e_ms, _ = host_time(lambda: P.accelerate(lambda e, o: P.hmm_kmer_forward(kmer, 0.5, 0.125, e, o), Ek, pobs),
                           1, 1, dist)
-    # algorithmic on-chip traffic per signal-step: alpha stay + step-predecessor
-    # reads, alpha write, emission row: 16 B per state (alpha stays L2-resident)
-    bytes_ = 16.0 * S * (T - 1) * nsig
+    # k = 8 runs on CTA pairs with alpha in registers (k_kmer_fwd_pair): what
+    # enters the SMs per signal-step is the emission row (4 B per state, an
+    # L2-resident table) plus the pair-sum exchange between the two CTAs (32 KiB
+    # each way, DSMEM, over the same xbar -> SM path); both are algorithmic.
+    emis = 4.0 * S
+    exch = 2.0 * 32768
+    bytes_ = (emis + exch) * T * nsig
     gbs = bytes_ / (ms * 1e-3) / 1e9
-    l2 = pipe_peaks().get("l2_3r1w_bytes_per_s_74MiB")
-    roof = {"bound": "l2", "unit": "GB/s", "achieved": round(gbs, 1), "bytes_per_signal_step": 16 * S,
-            "vs_hbm_peak": round(gbs / peaks["hbm_gbs"], 3),
+    l2 = pipe_peaks().get("l2_read_bytes_per_s_74MiB")
+    roof = {"bound": "sm ingress (L2 -> SM reads + DSMEM)", "unit": "GB/s", "achieved": round(gbs, 1),
+            "bytes_per_signal_step": emis + exch, "emission_bytes_per_signal_step": emis,
+            "dsmem_bytes_per_signal_step": exch, "vs_hbm_peak": round(gbs / peaks["hbm_gbs"], 3),
             "traffic": _kmer_traffic(T),
-            "note": "alpha (256 KiB per signal) double-buffered in an L2-resident slice per CTA; DRAM traffic is "
-                    "the fraction of alpha writes L2 evicts (profiles/traffic.json, ncu)"}
+            "note": "alpha never leaves the registers; ncu (T = 100): L2 reads = the emission rows once per "
+                    "signal-step, DRAM ~0, SM ingress = emissions + exchange (profiles/traffic.json). The DSMEM "
+                    "exchange alone runs at 17 B/clk/SM each way (tools/dsmem_probe.cu, profiles/r2_dsmem_probe.log)"}
     if l2:
         roof.update({"peak": round(l2 / 1e9, 1), "frac": round(gbs * 1e9 / l2, 4),
-                     "peak_source": "tools/l2_probe.cu: 3-read/1-write L2 stream over the kernel's 74 MiB footprint "
-                                    "(profiles/pipe_peaks.json l2_3r1w_bytes_per_s_74MiB)"})
+                     "peak_source": "tools/l2_probe.cu: read-only L2 -> SM stream, 148 SMs "
+                                    "(profiles/pipe_peaks.json l2_read_bytes_per_s_74MiB)"})
     res = {"value": NS / (ms * 1e-3), "ms_per_step": ms, "steps": s, "warmup": w,
            "trellis_cells_per_s": 5.0 * S * (T - 1) * NS / (ms * 1e-3),
            "e2e": _e2e("signals/s", NS, e2e_ms, pobs.numel() * 4 + 8 * Ek.size, 8 * nsig, pcie,
@@ -688,14 +694,16 @@ def bench_kmer(args, dist, peaks, pcie) -> dict:
 
 
 def _kmer_traffic(T: int):
-    """ncu L2 / DRAM bytes of one k-mer launch (1024 signals), scaled from the
-    T = 100 capture to T steps (per-step traffic is constant)."""
+    """ncu L2 / DRAM / SM-ingress bytes of one k-mer launch (1024 signals),
+    scaled from the T = 100 capture to T steps (per-step traffic is constant)."""
     t = _traffic_from_profiles("kmer")
     if not t:
         return None
-    f = (T - 1) / 99.0
+    f = T / 100.0
     return {"l2_bytes": t["l2_bytes_per_launch_T100"] * f, "dram_bytes": t["dram_bytes_per_launch_T100"] * f,
-            "l2_vs_algorithmic": round(t["l2_bytes_per_launch_T100"] / t["algorithmic_bytes_per_launch_T100"], 3),
+            "sm_ingress_bytes": t["sm_ingress_bytes_per_launch_T100"] * f,
+            "ingress_vs_algorithmic": round(t["sm_ingress_bytes_per_launch_T100"]
+                                            / t["algorithmic_bytes_per_launch_T100"], 3),
             "source": "profiles/traffic.json (ncu, T = 100, scaled)"}
 
 

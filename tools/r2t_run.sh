@@ -1,0 +1,14 @@
+# r2t: evidence refresh after the k-mer pair kernel: full GPU tests, smoke, bench (ours + reference
+# arm), launch list, ncu of the k-mer pair kernel, TMA-bulk L2 -> SM ingress probe
+mkdir -p gpurun_out
+./tools/l2_bulk_probe > gpurun_out/l2_bulk_probe.log 2>&1; cat gpurun_out/l2_bulk_probe.log
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+  --log-file gpurun_out/r2t_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-parity > gpurun_out/bench_ncu.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_kmer_fwd_pair -s 1 -c 1 -o gpurun_out/r2t_prof_kmer python tools/profile_cases.py kmer > /dev/null 2>&1
+ncu -i gpurun_out/r2t_prof_kmer.ncu-rep --page raw --csv > gpurun_out/r2t_kmer_raw.csv 2>/dev/null
+ls gpurun_out

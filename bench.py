@@ -665,7 +665,7 @@ def bench_kmer(args, dist, peaks, pcie) -> dict:
     exch = 2.0 * 32768
     bytes_ = (emis + exch) * T * nsig
     gbs = bytes_ / (ms * 1e-3) / 1e9
-    l2 = pipe_peaks().get("l2_read_bytes_per_s_74MiB")
+    l2 = pipe_peaks().get("l2_bulk_table_bytes_per_s")
     roof = {"bound": "sm ingress (L2 -> SM reads + DSMEM)", "unit": "GB/s", "achieved": round(gbs, 1),
             "bytes_per_signal_step": emis + exch, "emission_bytes_per_signal_step": emis,
             "dsmem_bytes_per_signal_step": exch, "vs_hbm_peak": round(gbs / peaks["hbm_gbs"], 3),
@@ -675,8 +675,9 @@ def bench_kmer(args, dist, peaks, pcie) -> dict:
                     "exchange alone runs at 17 B/clk/SM each way (tools/dsmem_probe.cu, profiles/r2_dsmem_probe.log)"}
     if l2:
         roof.update({"peak": round(l2 / 1e9, 1), "frac": round(gbs * 1e9 / l2, 4),
-                     "peak_source": "tools/l2_probe.cu: read-only L2 -> SM stream, 148 SMs "
-                                    "(profiles/pipe_peaks.json l2_read_bytes_per_s_74MiB)"})
+                     "peak_source": "tools/l2_bulk_probe.cu: TMA bulk copies of one 2 MiB L2-resident table into "
+                                    "every SM (profiles/pipe_peaks.json l2_bulk_table_bytes_per_s; the ld.global "
+                                    "probe reaches 12.5 TB/s)"})
     res = {"value": NS / (ms * 1e-3), "ms_per_step": ms, "steps": s, "warmup": w,
            "trellis_cells_per_s": 5.0 * S * (T - 1) * NS / (ms * 1e-3),
            "e2e": _e2e("signals/s", NS, e2e_ms, pobs.numel() * 4 + 8 * Ek.size, 8 * nsig, pcie,

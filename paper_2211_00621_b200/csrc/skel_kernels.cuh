@@ -664,11 +664,35 @@ k_seq_loop_jit(const F f, const double* src, double* a, double* b, int64_t m, in
     fl.T[0].rank = 1;
     fl.T[0].dtype = PMX_F64;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // straight-line bodies: SQU = 8 elements per thread per pass (grid-strided, so
+    // each of the SQU loads is coalesced across the warp), all loads and the
+    // body's reads of the previous state issued before the stores
+    constexpr int SQU = F::kStraight ? 8 : 1;
     for (int64_t t = 0; t < steps; ++t) {
         const double* cur = t == 0 ? src : ((t & 1) ? b : a);   // step 0 reads the caller's state
         double* nxt = (t & 1) ? a : b;
         fl.T[0].data = const_cast<double*>(cur);
-        for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
+        int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (SQU > 1) {
+            for (; j + (SQU - 1) * stride < m; j += SQU * stride) {
+                int64_t x[SQU], jj[SQU], tt[SQU], o[SQU];
+                int code[SQU];
+#pragma unroll
+                for (int u = 0; u < SQU; ++u) {
+                    jj[u] = j + u * stride;
+                    x[u] = __double_as_longlong(__ldcg(cur + jj[u]));
+                    tt[u] = t;
+                    code[u] = 0;
+                }
+                fl.template run<SQU>(x, jj, tt, o, code);
+#pragma unroll
+                for (int u = 0; u < SQU; ++u) {
+                    if (code[u]) raise_err(err, jj[u], code[u]);
+                    nxt[jj[u]] = F::kOutFloat ? __longlong_as_double(o[u]) : (double)o[u];
+                }
+            }
+        }
+        for (; j < m; j += stride) {
             const int64_t x[1] = {__double_as_longlong(__ldcg(cur + j))}, jj[1] = {j}, tt[1] = {t};
             int64_t o[1];
             int code[1] = {0};

@@ -388,13 +388,15 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         const uint64_t b_desc0 = main_desc(S.B[0]);
         const uint64_t aaug_desc = tc::sw32_kmajor_desc(tc::smem_u32(S.Aaug));
         const uint64_t baug_desc0 = tc::sw32_kmajor_desc(tc::smem_u32(S.Baug[0]));
+        const uint32_t full_a = tc::smem_u32(&S.full[0]), empty_a = tc::smem_u32(&S.empty[0]);
+        const uint32_t tfull_a = tc::smem_u32(&S.tfull[0]), tempty_a = tc::smem_u32(&S.tempty[0]);
         for (int it = it_begin; it < it_end; ++it) {
             const int sp = it % nsplit;
             const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
             tc::mbar_wait(&S.a_full, a_par); a_par ^= 1;
             for (int t = t0; t < t1; ++t) {
-                tc::mbar_wait(&S.tempty[b], acc_phase ^ 1);
-                tc::mbar_wait(&S.full[stage], phase);
+                tc::mbar_wait_addr(tempty_a + 8u * b, acc_phase ^ 1);
+                tc::mbar_wait_addr(full_a + 8u * stage, phase);
                 tc::tc_fence_after();
                 if (tc::elect_one()) {
                     const uint64_t bd = b_desc0 + (uint64_t)(stage * (B_BYTES >> 4));
@@ -414,8 +416,8 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                         if (Ops::ROWB == 128) tc::umma_f16(d, aad, bad, idesc, 1);
                         else tc::umma_i8(d, aad, bad, idesc, 1);
                     }
-                    tc::umma_commit(&S.empty[stage]);
-                    tc::umma_commit(&S.tfull[b]);
+                    tc::umma_commit_addr(empty_a + 8u * stage);
+                    tc::umma_commit_addr(tfull_a + 8u * b);
                 }
                 __syncwarp();
                 if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
@@ -430,6 +432,10 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         const int quad = warp & 3, h = (ew >> 2) & 1, ch = ew >> 3;
         const int row = h * KT_M + quad * 32 + lane;           // query within the block
         int b = 0; uint32_t acc_phase = 0;
+        // shared addresses of the accumulator barriers, once (the smem struct is
+        // reached through a generic pointer: converting it per tile costs an
+        // S2UR of the CTA id and address arithmetic on every wait / arrive)
+        const uint32_t tfull_a = tc::smem_u32(&S.tfull[0]), tempty_a = tc::smem_u32(&S.tempty[0]);
         Top8 L;
         int prev_qb = -1;
         uint32_t pseudo = KT_EMPTY;
@@ -441,7 +447,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
             else pseudo = L.carry();
             prev_qb = qb;
             for (int t = t0; t < t1; ++t) {
-                tc::mbar_wait(&S.tfull[b], acc_phase);
+                tc::mbar_wait_addr(tfull_a + 8u * b, acc_phase);
                 tc::tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((b * 2 + h) * KT_N + ch * 64);
                 uint32_t r[32];
@@ -452,7 +458,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                 // until it falls a whole tile behind)
                 tc::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&S.tempty[b]);
+                if (lane == 0) tc::mbar_arrive_addr(tempty_a + 8u * b);
                 if (t == ntiles - 1) {                       // last tile: padded rows never enter
                     const int64_t colbase = (int64_t)t * KT_N + ch * 64;
 #pragma unroll

@@ -25,7 +25,9 @@
 //            bf16 of -2x) + B_aug (128 x 16) through a 4-stage ring
 //   warp 1   TMEM allocator and MMA issuer (one thread): per train tile, two
 //            128 x 128 accumulators (one per 128-query half) into one of two
-//            TMEM buffers (2 buffers x 2 halves x 128 columns = all 512 columns)
+//            TMEM buffers (2 buffers x 2 halves x 128 columns = all 512 columns);
+//            each half has its own full / empty barriers, so the two groups of
+//            8 epilogue warps never wait for each other
 //   warps 2-17 epilogue: warp w owns TMEM lane quadrant w%4 (one query per
 //            thread), query half ((w-2)>>2)&1 and column half (w-2)>>3; it
 //            loads its 64 candidates of the tile (one packed tcgen05.ld),
@@ -91,7 +93,7 @@ struct __align__(1024) KnnSmem {
     uint8_t Baug[KT_STAGES][KT_N * KT_AUGB];
     uint64_t full[KT_STAGES], empty[KT_STAGES];
     uint64_t a_full, a_empty;
-    uint64_t tfull[2], tempty[2];
+    uint64_t tfull[2][2], tempty[2][2];   // [buffer][query half]
     uint32_t tmem_base;
 };
 
@@ -340,7 +342,8 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         for (int s = 0; s < KT_STAGES; ++s) { tc::mbar_init(&S.full[s], 1); tc::mbar_init(&S.empty[s], 1); }
         tc::mbar_init(&S.a_full, 1);
         tc::mbar_init(&S.a_empty, 1);
-        for (int b = 0; b < 2; ++b) { tc::mbar_init(&S.tfull[b], 1); tc::mbar_init(&S.tempty[b], KT_EW); }
+        for (int b = 0; b < 2; ++b)
+            for (int h = 0; h < 2; ++h) { tc::mbar_init(&S.tfull[b][h], 1); tc::mbar_init(&S.tempty[b][h], KT_EW / 2); }
         tc::fence_mbar_init();
         tc::tma_prefetch(&tmq);
         tc::tma_prefetch(&tmqa);
@@ -389,20 +392,23 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         const uint64_t aaug_desc = tc::sw32_kmajor_desc(tc::smem_u32(S.Aaug));
         const uint64_t baug_desc0 = tc::sw32_kmajor_desc(tc::smem_u32(S.Baug[0]));
         const uint32_t full_a = tc::smem_u32(&S.full[0]), empty_a = tc::smem_u32(&S.empty[0]);
-        const uint32_t tfull_a = tc::smem_u32(&S.tfull[0]), tempty_a = tc::smem_u32(&S.tempty[0]);
+        const uint32_t tfull_a = tc::smem_u32(&S.tfull[0][0]), tempty_a = tc::smem_u32(&S.tempty[0][0]);
         for (int it = it_begin; it < it_end; ++it) {
             const int sp = it % nsplit;
             const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
             tc::mbar_wait(&S.a_full, a_par); a_par ^= 1;
             for (int t = t0; t < t1; ++t) {
-                tc::mbar_wait_addr(tempty_a + 8u * b, acc_phase ^ 1);
                 tc::mbar_wait_addr(full_a + 8u * stage, phase);
-                tc::tc_fence_after();
-                if (tc::elect_one()) {
-                    const uint64_t bd = b_desc0 + (uint64_t)(stage * (B_BYTES >> 4));
-                    const uint64_t bad = baug_desc0 + (uint64_t)(stage * (BAUG_BYTES >> 4));
+                const uint64_t bd = b_desc0 + (uint64_t)(stage * (B_BYTES >> 4));
+                const uint64_t bad = baug_desc0 + (uint64_t)(stage * (BAUG_BYTES >> 4));
+                // per query half: its accumulator free (its 8 epilogue warps), its
+                // UMMAs, its own commit — the halves' epilogue groups do not wait
+                // for each other
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < 2; ++h) {
+                    tc::mbar_wait_addr(tempty_a + 16u * b + 8u * h, acc_phase ^ 1);
+                    tc::tc_fence_after();
+                    if (tc::elect_one()) {
                         const uint32_t d = tmem + (uint32_t)((b * 2 + h) * KT_N);
                         const uint64_t ad = a_desc + (uint64_t)(h * ((KT_M * Ops::ROWB) >> 4));
                         // K advances 32 bytes (2 descriptor units) per UMMA
@@ -415,11 +421,11 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                         const uint64_t aad = aaug_desc + (uint64_t)(h * ((KT_M * KT_AUGB) >> 4));
                         if (Ops::ROWB == 128) tc::umma_f16(d, aad, bad, idesc, 1);
                         else tc::umma_i8(d, aad, bad, idesc, 1);
+                        tc::umma_commit_addr(tfull_a + 16u * b + 8u * h);
+                        if (h == 1) tc::umma_commit_addr(empty_a + 8u * stage);
                     }
-                    tc::umma_commit_addr(empty_a + 8u * stage);
-                    tc::umma_commit_addr(tfull_a + 8u * b);
+                    __syncwarp();
                 }
-                __syncwarp();
                 if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
                 b ^= 1;
                 if (b == 0) acc_phase ^= 1;
@@ -435,7 +441,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         // shared addresses of the accumulator barriers, once (the smem struct is
         // reached through a generic pointer: converting it per tile costs an
         // S2UR of the CTA id and address arithmetic on every wait / arrive)
-        const uint32_t tfull_a = tc::smem_u32(&S.tfull[0]), tempty_a = tc::smem_u32(&S.tempty[0]);
+        const uint32_t tfull_a = tc::smem_u32(&S.tfull[0][h]), tempty_a = tc::smem_u32(&S.tempty[0][h]);
         Top8 L;
         int prev_qb = -1;
         uint32_t pseudo = KT_EMPTY;
@@ -447,7 +453,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
             else pseudo = L.carry();
             prev_qb = qb;
             for (int t = t0; t < t1; ++t) {
-                tc::mbar_wait_addr(tfull_a + 8u * b, acc_phase);
+                tc::mbar_wait_addr(tfull_a + 16u * b, acc_phase);
                 tc::tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((b * 2 + h) * KT_N + ch * 64);
                 uint32_t r[32];
@@ -458,7 +464,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                 // until it falls a whole tile behind)
                 tc::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive_addr(tempty_a + 8u * b);
+                if (lane == 0) tc::mbar_arrive_addr(tempty_a + 16u * b);
                 if (t == ntiles - 1) {                       // last tile: padded rows never enter
                     const int64_t colbase = (int64_t)t * KT_N + ch * 64;
 #pragma unroll

@@ -72,15 +72,20 @@ constexpr int KT_LPQ = 2;                 // partial lists per query per item (c
 // 32-byte augmentation row (SWIZZLE_32B).  Every UMMA consumes 32 bytes of K.
 //   BF16: kind::f16, fp32 accumulation, D = dist + 2^23 (low 16 bits = dist)
 //   I8:   kind::i8, int32 accumulation, D = dist (exact by construction)
+#ifndef KT_SPLIT
+#define KT_SPLIT 1                        // accumulator regions per query half (N = 128 / KT_SPLIT per UMMA; 2: 10.0 ms)
+#endif
+constexpr int KT_NU = KT_N / KT_SPLIT;    // UMMA N
 struct OpsBF16 {
     static constexpr int ROWB = 128, KSTEPS = 4;
-    static constexpr uint32_t IDESC = tc::instr_desc(128, 128, 1);
+    static constexpr uint32_t IDESC = tc::instr_desc(128, KT_NU, 1);
     static constexpr unsigned FLAG_RUN = 8;       // runs when only the int8 form is inexact
 };
 struct OpsI8 {
     static constexpr int ROWB = 64, KSTEPS = 2;
     // c_format S32 (2), a/b signed int8 (1), K-major, N >> 3, M >> 4
-    static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+    static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (((uint32_t)KT_NU >> 3) << 17) |
+                                      ((128u >> 4) << 24);
     static constexpr unsigned FLAG_RUN = 0;
 };
 constexpr int KT_AUGB = 32;                       // augmentation row bytes (16 bf16 / 32 int8)
@@ -93,7 +98,7 @@ struct __align__(1024) KnnSmem {
     uint8_t Baug[KT_STAGES][KT_N * KT_AUGB];
     uint64_t full[KT_STAGES], empty[KT_STAGES];
     uint64_t a_full, a_empty;
-    uint64_t tfull[2][2], tempty[2][2];   // [buffer][query half]
+    uint64_t tfull[2][2][KT_SPLIT], tempty[2][2][KT_SPLIT];   // [buffer][query half][column region]
     uint32_t tmem_base;
 };
 
@@ -343,7 +348,11 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         tc::mbar_init(&S.a_full, 1);
         tc::mbar_init(&S.a_empty, 1);
         for (int b = 0; b < 2; ++b)
-            for (int h = 0; h < 2; ++h) { tc::mbar_init(&S.tfull[b][h], 1); tc::mbar_init(&S.tempty[b][h], KT_EW / 2); }
+            for (int h = 0; h < 2; ++h)
+                for (int c = 0; c < KT_SPLIT; ++c) {
+                    tc::mbar_init(&S.tfull[b][h][c], 1);
+                    tc::mbar_init(&S.tempty[b][h][c], KT_EW / (2 * KT_SPLIT));
+                }
         tc::fence_mbar_init();
         tc::tma_prefetch(&tmq);
         tc::tma_prefetch(&tmqa);
@@ -392,7 +401,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         const uint64_t aaug_desc = tc::sw32_kmajor_desc(tc::smem_u32(S.Aaug));
         const uint64_t baug_desc0 = tc::sw32_kmajor_desc(tc::smem_u32(S.Baug[0]));
         const uint32_t full_a = tc::smem_u32(&S.full[0]), empty_a = tc::smem_u32(&S.empty[0]);
-        const uint32_t tfull_a = tc::smem_u32(&S.tfull[0][0]), tempty_a = tc::smem_u32(&S.tempty[0][0]);
+        const uint32_t tfull_a = tc::smem_u32(&S.tfull[0][0][0]), tempty_a = tc::smem_u32(&S.tempty[0][0][0]);
         for (int it = it_begin; it < it_end; ++it) {
             const int sp = it % nsplit;
             const int t0 = (int)((int64_t)sp * ntiles / nsplit), t1 = (int)((int64_t)(sp + 1) * ntiles / nsplit);
@@ -405,27 +414,32 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                 // UMMAs, its own commit — the halves' epilogue groups do not wait
                 // for each other
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    tc::mbar_wait_addr(tempty_a + 16u * b + 8u * h, acc_phase ^ 1);
-                    tc::tc_fence_after();
-                    if (tc::elect_one()) {
-                        const uint32_t d = tmem + (uint32_t)((b * 2 + h) * KT_N);
-                        const uint64_t ad = a_desc + (uint64_t)(h * ((KT_M * Ops::ROWB) >> 4));
-                        // K advances 32 bytes (2 descriptor units) per UMMA
+                for (int h = 0; h < 2; ++h)
 #pragma unroll
-                        for (int kk = 0; kk < Ops::KSTEPS; ++kk) {
-                            if (Ops::ROWB == 128) tc::umma_f16(d, ad + 2 * kk, bd + 2 * kk, idesc, kk > 0);
-                            else tc::umma_i8(d, ad + 2 * kk, bd + 2 * kk, idesc, kk > 0);
+                    for (int c = 0; c < KT_SPLIT; ++c) {
+                        const uint32_t bo = 8u * ((b * 2 + h) * KT_SPLIT + c);
+                        tc::mbar_wait_addr(tempty_a + bo, acc_phase ^ 1);
+                        tc::tc_fence_after();
+                        if (tc::elect_one()) {
+                            const uint32_t d = tmem + (uint32_t)((b * 2 + h) * KT_N + c * KT_NU);
+                            const uint64_t ad = a_desc + (uint64_t)(h * ((KT_M * Ops::ROWB) >> 4));
+                            const uint64_t bdc = bd + (uint64_t)(c * ((KT_NU * Ops::ROWB) >> 4));
+                            const uint64_t badc = bad + (uint64_t)(c * ((KT_NU * KT_AUGB) >> 4));
+                            // K advances 32 bytes (2 descriptor units) per UMMA
+#pragma unroll
+                            for (int kk = 0; kk < Ops::KSTEPS; ++kk) {
+                                if (Ops::ROWB == 128) tc::umma_f16(d, ad + 2 * kk, bdc + 2 * kk, idesc, kk > 0);
+                                else tc::umma_i8(d, ad + 2 * kk, bdc + 2 * kk, idesc, kk > 0);
+                            }
+                            // + ||x||^2 + ||q||^2 (+ 2^23 for the bf16 form)
+                            const uint64_t aad = aaug_desc + (uint64_t)(h * ((KT_M * KT_AUGB) >> 4));
+                            if (Ops::ROWB == 128) tc::umma_f16(d, aad, badc, idesc, 1);
+                            else tc::umma_i8(d, aad, badc, idesc, 1);
+                            tc::umma_commit_addr(tfull_a + bo);
+                            if (h == 1 && c == KT_SPLIT - 1) tc::umma_commit_addr(empty_a + 8u * stage);
                         }
-                        // + ||x||^2 + ||q||^2 (+ 2^23 for the bf16 form)
-                        const uint64_t aad = aaug_desc + (uint64_t)(h * ((KT_M * KT_AUGB) >> 4));
-                        if (Ops::ROWB == 128) tc::umma_f16(d, aad, bad, idesc, 1);
-                        else tc::umma_i8(d, aad, bad, idesc, 1);
-                        tc::umma_commit_addr(tfull_a + 16u * b + 8u * h);
-                        if (h == 1) tc::umma_commit_addr(empty_a + 8u * stage);
+                        __syncwarp();
                     }
-                    __syncwarp();
-                }
                 if (++stage == KT_STAGES) { stage = 0; phase ^= 1; }
                 b ^= 1;
                 if (b == 0) acc_phase ^= 1;
@@ -441,7 +455,9 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
         // shared addresses of the accumulator barriers, once (the smem struct is
         // reached through a generic pointer: converting it per tile costs an
         // S2UR of the CTA id and address arithmetic on every wait / arrive)
-        const uint32_t tfull_a = tc::smem_u32(&S.tfull[0][h]), tempty_a = tc::smem_u32(&S.tempty[0][h]);
+        // my 64 columns lie in column region ch * 64 / KT_NU of my half
+        const uint32_t tfull_a = tc::smem_u32(&S.tfull[0][h][ch * 64 / KT_NU]),
+                       tempty_a = tc::smem_u32(&S.tempty[0][h][ch * 64 / KT_NU]);
         Top8 L;
         int prev_qb = -1;
         uint32_t pseudo = KT_EMPTY;
@@ -453,7 +469,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
             else pseudo = L.carry();
             prev_qb = qb;
             for (int t = t0; t < t1; ++t) {
-                tc::mbar_wait_addr(tfull_a + 16u * b, acc_phase);
+                tc::mbar_wait_addr(tfull_a + 8u * (2 * KT_SPLIT) * b, acc_phase);
                 tc::tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((b * 2 + h) * KT_N + ch * 64);
                 uint32_t r[32];
@@ -464,7 +480,7 @@ k_knn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtens
                 // until it falls a whole tile behind)
                 tc::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive_addr(tempty_a + 16u * b);
+                if (lane == 0) tc::mbar_arrive_addr(tempty_a + 8u * (2 * KT_SPLIT) * b);
                 if (t == ntiles - 1) {                       // last tile: padded rows never enter
                     const int64_t colbase = (int64_t)t * KT_N + ch * 64;
 #pragma unroll

@@ -306,6 +306,7 @@ k_viterbi_pruned(const double* __restrict__ log_pi, const double* __restrict__ l
     __shared__ int s_sym[VP_MS];
     __shared__ double s_red[VP_NT / 32][VP_MS];
     __shared__ double s_M[VP_MS];
+    __shared__ int s_next;                 // next group of 4 target states (dynamic, per step)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int m = lane & 7, g = lane >> 3;
     const int64_t s0 = (int64_t)blockIdx.x * VP_MS;
@@ -321,6 +322,7 @@ k_viterbi_pruned(const double* __restrict__ log_pi, const double* __restrict__ l
     __syncthreads();
     for (int t = 1; t < T; ++t) {
         if (tid < VP_MS) s_sym[tid] = s0 + tid < nsig ? obs[(s0 + tid) * T + t] : 0;
+        if (tid == 0) s_next = 0;
         // M = max_i chi[i] per signal
         double mx = NEG_INF;
         for (int i = tid >> 3; i < S; i += VP_NT / 8) mx = fmax(mx, cur[i * VP_MS + (tid & 7)]);
@@ -336,8 +338,14 @@ k_viterbi_pruned(const double* __restrict__ log_pi, const double* __restrict__ l
         __syncthreads();
         const double M = s_M[m];
         const int o = s_sym[m];
-        for (int jb = 0; jb < S; jb += 4 * (VP_NT / 32)) {
-            const int j = jb + warp * 4 + g;
+        // groups of 4 target states handed out dynamically: scans stop at different
+        // ranks, so a static split leaves warps idle at the step's barrier
+        for (;;) {
+            int jg = 0;
+            if (lane == 0) jg = atomicAdd(&s_next, 1);
+            jg = __shfl_sync(0xffffffffu, jg, 0);
+            if (jg >= S / 4) break;
+            const int j = jg * 4 + g;
             const double* col = lAs + (int64_t)j * S;
             const uint16_t* pc = perm + (int64_t)j * S;
             double best = NEG_INF;

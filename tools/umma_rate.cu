@@ -86,6 +86,10 @@ int main() {
     run<64>(sms);
     run<128>(sms);
     run<256>(sms);
+    run<64, true>(sms);
+    run<80, true>(sms);
+    run<96, true>(sms);
+    run<112, true>(sms);
     run<128, true>(sms);
     run<256, true>(sms);
     return 0;

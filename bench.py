@@ -247,9 +247,11 @@ def cpu_threads() -> int:
     return max(1, len(os.sched_getaffinity(0)))
 
 
-def pcie_h2d_gbs(nbytes: int = 1 << 28) -> float:
-    """Pinned host -> device copy bandwidth (GB/s, best of 5): the bound of
-    any end-to-end number whose inputs start in host memory."""
+def pcie_h2d_gbs(nbytes: int = 1 << 30) -> float:
+    """Pinned host -> device copy bandwidth (GB/s, best of 6) at the headline's
+    1 GiB: the bound of any end-to-end number whose inputs start in host
+    memory (tools/h2d_probe.py: one stream or the bytes split over 2 / 4
+    streams copy at the same 55.5 GB/s, i.e. the link, not a copy engine)."""
     import torch
     h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")

@@ -225,6 +225,27 @@ def test_seq_loop_specialised_persistent_kernel():
     assert "element 4242)" in str(ei.value)
 
 
+def test_seq_loop_multi_lane_passes_and_tail():
+    # m large enough that the specialised kernel runs its 8-elements-per-thread
+    # passes (grid-strided) and then a ragged scalar tail; an error raised in two
+    # elements of the multi-lane region reports the smaller one
+    m, steps = (1 << 22) + 3, 3
+    s0 = np.arange(m, dtype=np.float64) % 89
+    step = P.lam("x", "j", "t", P.addf(P.mulf(0.5, P.addf("x", P.get(P.PREV, P.modi(P.addi("j", 7), m)))),
+                                       P.mulf(0.25, P.int2float(P.modi("j", 5)))))
+    got = np.asarray(P.accelerate(lambda s: P.seq_loop(steps, step, s), s0))
+    want = s0.copy()
+    jm = (np.arange(m) % 5).astype(np.float64)
+    for _ in range(steps):
+        want = 0.5 * (want + np.roll(want, -7)) + 0.25 * jm
+    assert np.array_equal(got, want)
+    # straight-line (so the multi-lane path runs it): zero divisor at two elements
+    bad = P.lam("x", "j", "t", P.divf("x", P.int2float(P.muli(P.subi("j", 1_000_003), P.subi("j", 3_000_017)))))
+    with pytest.raises(P.Diagnostics, match="float division by zero") as ei:
+        P.accelerate(lambda s: P.seq_loop(steps, bad, s), s0)
+    assert "element 1000003)" in str(ei.value)
+
+
 def test_reduce_unrecognised_operator_is_an_ordered_fold():
     # leftmost non-zero: associative, not commutative -> only an order-keeping
     # tree gives the sequential answer

@@ -30,6 +30,14 @@ int sm_count();                                  // cached per device
 
 inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
+// log of a forward step's scale c_t (or a product of them) for the running
+// log-likelihood of the HMM kernels.  c = 0 (an observation no state can emit,
+// with log-space inputs of -inf) gives NaN, as the reference's log-space
+// recursion does: its max-shifted log-sum-exp over all -inf terms is NaN.
+__device__ __forceinline__ double log_scale(double c) {
+    return c > 0.0 ? log(c) : __longlong_as_double(0x7ff8000000000000ll);
+}
+
 inline size_t dtype_size(int dt) {
     switch (dt) {
         case PMX_F32: case PMX_I32: return 4;

@@ -76,7 +76,7 @@ __global__ void k_hmm_fwd_small(const float* __restrict__ pi_lin, const float* _
             float c = 0.f;
             for (int w = 0; w < (int)((blockDim.x + 31) >> 5); ++w) c += s_red[w];
             s_c = c;
-            ll += log((double)c);
+            ll += log_scale((double)c);
         }
         __syncthreads();
         const float inv = 1.0f / s_c;
@@ -222,7 +222,7 @@ k_hmm_fwd_tiled(const float* __restrict__ pi_lin, const float* __restrict__ A,
             float c = 0.f;
             for (int w = g * (GT / 32); w < (g + 1) * (GT / 32); ++w) c += s_red[w][a];
             s_inv[tid] = 1.0f / c;
-            ll += log((double)c);
+            ll += log_scale((double)c);
         }
         __syncthreads();
         // ahat_t -> aT (transposed: 8 signals contiguous per state)

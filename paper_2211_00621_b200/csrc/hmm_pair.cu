@@ -356,7 +356,7 @@ k_hmm_fwd_pair(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 // own + peer, added in rank order so both CTAs get the same c_t
                 const float c = (rank == 0 ? part + Sm.psum_in[t & 1][m] : Sm.psum_in[t & 1][m] + part) * kSum;
                 Sm.inv_c[m] = 1.f / c;
-                ll += log((double)c);
+                ll += log_scale((double)c);
             }
             spar ^= 1;
             asm volatile("bar.sync 1, %0;" :: "n"(32 * HP_EW) : "memory");

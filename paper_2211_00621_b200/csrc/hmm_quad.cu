@@ -265,7 +265,7 @@ k_hmm_fwd_quad(const __grid_constant__ CUtensorMap tmA, const float* __restrict_
                 // budget; such a signal is re-run by the fp32 kernel.
                 if (!(c >= 0.00390625f)) out_of_range = true;
                 cprod *= (double)c;                          // one fp64 log per 16 steps
-                if ((tt & 15) == 15 || tt == T - 1) { ll += log(cprod); cprod = 1.0; }
+                if ((tt & 15) == 15 || tt == T - 1) { ll += log_scale(cprod); cprod = 1.0; }
             }
             asm volatile("bar.sync 1, %0;" :: "n"(32 * HQ_EW) : "memory");
         };

@@ -295,7 +295,7 @@ k_hmm_fwd_tc(const __grid_constant__ CUtensorMap tmA, const float* __restrict__ 
             if (ew == 0) {
                 const float c = (Sm.wsum[0][lane] + Sm.wsum[1][lane] + Sm.wsum[2][lane] + Sm.wsum[3][lane]) * EL::kSum;
                 Sm.inv_c[lane] = 1.f / c;
-                ll += log((double)c);
+                ll += log_scale((double)c);
             }
             asm volatile("bar.sync 1, 256;" ::: "memory");
             if (threadIdx.x == 128 && t + 1 < T) {

@@ -78,7 +78,7 @@ k_kmer_fwd(int kmer, float p_stay, float p_step, const float* __restrict__ E_lin
                 float c = 0.f;
                 for (int w = 0; w < (int)(blockDim.x >> 5); ++w) c += s_red[w];
                 s_c = c;
-                ll += log((double)c);
+                ll += log_scale((double)c);
             }
             __syncthreads();
             inv = 1.0f / s_c;
@@ -185,7 +185,7 @@ k_kmer_fwd_vec(int kmer, float p_stay, float p_step, const float* __restrict__ E
                 float c = 0.f;
                 for (int w = 0; w < (int)(blockDim.x >> 5); ++w) c += s_red[w];
                 s_c = c;
-                ll += log((double)c);
+                ll += log_scale((double)c);
             }
             __syncthreads();
             inv = 1.0f / s_c;
@@ -347,7 +347,7 @@ __device__ __forceinline__ void pair_run(Smem& sm, float p_stay, float p_step, c
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
                 if (R == 0 && tid == 0) {
-                    ll += log((double)c);
+                    ll += log_scale((double)c);
                     if (t == 0) { out_ll[prev] = ll; ll = 0.0; }
                 }
                 if (t > 0) inv = 1.0f / c;
@@ -404,7 +404,7 @@ __device__ __forceinline__ void pair_run(Smem& sm, float p_stay, float p_step, c
         float c = sm.part[ps][lane >> 4][lane & 15];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
-        if (R == 0 && tid == 0) out_ll[prev] = ll + log((double)c);
+        if (R == 0 && tid == 0) out_ll[prev] = ll + log_scale((double)c);
     }
 }
 }  // namespace kp

@@ -9,6 +9,7 @@ import pytest
 import torch
 
 import oracle as O
+import paper_2211_00621_b200 as P
 from paper_2211_00621_b200 import (
     accelerate, hmm_forward, hmm_kmer_forward, knn_classify, rk4_sweep, synth, viterbi,
 )
@@ -100,6 +101,51 @@ def test_hmm_forward_tensor_core_path_precision():
     want = O.hmm_forward(A, E, pi, obs)
     err = np.max(np.abs(got - want) / np.abs(want))
     assert err < 5e-6, err
+
+
+def _impossible_symbol_obs(nsig, T):
+    obs = synth.hmm_obs(nsig, T, 8) % 7
+    obs[1, 4] = 7          # symbol 7 mid-sequence, at the first step and at the last
+    obs[2, 0] = 7
+    obs[nsig - 1, T - 1] = 7
+    return obs
+
+
+@pytest.mark.parametrize("S", [64, 1024])
+def test_hmm_forward_zero_emission_probability_raises_like_reference(S):
+    # the program takes log of the probabilities: log 0.0 is the reference's
+    # "math domain error" (pmx/interp.py scalar semantics), raised here too
+    A, E, pi = synth.hmm_model(S, 8)
+    E = E.copy()
+    E[:, 7] = 0.0
+    with pytest.raises(P.Diagnostics, match="log: math domain error"):
+        accelerate(hmm_forward, A, E, pi, _impossible_symbol_obs(5, 9))
+
+
+@pytest.mark.parametrize("S", [64, 256, 1024])
+def test_hmm_forward_raw_impossible_observation_is_nan(S):
+    # the C-ABI entry with log-space inputs (log E = -inf for symbol 7): a signal
+    # that observes it gets NaN, as the log-space recursion does (its
+    # max-shifted log-sum-exp over all -inf terms); other signals are unaffected
+    A, E, pi = synth.hmm_model(S, 8)
+    E = E.copy()
+    E[:, 7] = 0.0
+    obs = _impossible_symbol_obs(5, 9)
+    nsig, T = obs.shape
+    with np.errstate(divide="ignore", invalid="ignore"):
+        want = O.hmm_forward(A, E, pi, obs)
+        lE = torch.from_numpy(np.log(E).astype(np.float32)).cuda()
+        lpi = torch.from_numpy(np.log(pi).astype(np.float32)).cuda()
+    Ad = torch.from_numpy(A.astype(np.float32)).cuda()
+    o = torch.from_numpy(obs.astype(np.int32)).cuda()
+    out = torch.empty(nsig, dtype=torch.float64, device="cuda")
+    from paper_2211_00621_b200 import _lib, casestudies as CS
+    ws = torch.empty(_lib.load().pmx_hmm_forward_workspace_bytes(S, nsig), dtype=torch.uint8, device="cuda")
+    CS.hmm_forward_raw(lpi, Ad, lE, o, S, 8, nsig, T, out, ws)
+    got = out.cpu().numpy()
+    assert np.isnan(want[[1, 2, 4]]).all()
+    assert np.isnan(got[[1, 2, 4]]).all(), got
+    assert np.allclose(got[[0, 3]], want[[0, 3]], rtol=LL_REL, atol=0)
 
 
 def test_hmm_forward_long_sequence_precision():
@@ -287,6 +333,35 @@ def test_kmer8_cluster_signal_loop(nsig, T):
     got = accelerate(lambda em, o: hmm_kmer_forward(8, 0.5, 0.125, em, o), E, obs)
     want = O.kmer_forward_scaled(8, 0.5, 0.125, E, obs)
     assert np.allclose(got, want, rtol=LL_REL, atol=0)
+
+
+@pytest.mark.parametrize("kmer", [4, 8])
+def test_kmer_raw_impossible_observation_is_nan(kmer):
+    # C-ABI entry with log E = -inf for symbol 7 in every state: a signal that
+    # observes it gets NaN like the log-space recursion; through accelerate the
+    # program's log 0.0 raises the reference's math domain error instead
+    S, K = 1 << (2 * kmer), 8
+    E = synth.kmer_emission(kmer, K)
+    E[:, 7] = 0.0
+    obs = _impossible_symbol_obs(5, 12)
+    nsig, T = obs.shape
+    with np.errstate(divide="ignore", invalid="ignore"):
+        want = O.kmer_forward(kmer, 0.5, 0.125, E, obs)
+        lE = torch.from_numpy(np.log(E).astype(np.float32)).cuda()
+    from paper_2211_00621_b200 import _lib
+    lib = _lib.load()
+    o = torch.from_numpy(obs.astype(np.int32)).cuda()
+    out = torch.empty(nsig, dtype=torch.float64, device="cuda")
+    ws = torch.empty(lib.pmx_hmm_kmer_workspace_bytes(kmer, nsig), dtype=torch.uint8, device="cuda")
+    _lib.check(lib.pmx_hmm_kmer_forward_f32(kmer, 0.5, 0.125, lE.data_ptr(), K, o.data_ptr(), nsig, T,
+                                            out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                            torch.cuda.current_stream().cuda_stream), "kmer")
+    got = out.cpu().numpy()
+    assert np.isnan(want[[1, 2, 4]]).all()
+    assert np.isnan(got[[1, 2, 4]]).all(), got
+    assert np.allclose(got[[0, 3]], want[[0, 3]], rtol=LL_REL, atol=0)
+    with pytest.raises(P.Diagnostics, match="log: math domain error"):
+        accelerate(lambda em, ob: hmm_kmer_forward(kmer, 0.5, 0.125, em, ob), E, obs)
 
 
 def test_kmer8_cluster_peaked_emissions():

@@ -1,8 +1,7 @@
 """Time the k-NN kernels at the BASELINE config (2^20 train x 2^16 queries,
 d = 64, k = 8) through pmx_knn_f32 with device-resident inputs; print the
-median ms.  PMX_KNN_PROBE=1|2 times the tensor-core kernel with its scan
-(1) or its TMEM loads and scan (2) removed (results then wrong): the
-MMA + TMEM-read pipeline alone, and the MMA + TMA pipeline alone."""
+median ms.  (The r1 PMX_KNN_PROBE pipeline-only variants were removed from
+the kernel; the variable is only echoed for old logs.)"""
 import os
 import sys
 

@@ -669,6 +669,9 @@ def _force(v):
 
 
 def _takes_ctx(fn) -> bool:
+    code = getattr(fn, "__code__", None)
+    if code is not None and not hasattr(fn, "__wrapped__"):   # plain function / lambda: no inspect
+        return "ctx" in code.co_varnames[:code.co_argcount + code.co_kwonlyargcount]
     import inspect
     try:
         return "ctx" in inspect.signature(fn).parameters

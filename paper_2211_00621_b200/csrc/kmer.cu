@@ -218,13 +218,17 @@ k_kmer_fwd_vec(int kmer, float p_stay, float p_step, const float* __restrict__ E
 // __syncthreads: one mbarrier per receive slot (two slots by step parity)
 // counts the 512 threads' arrivals plus the peer's bytes.
 namespace kp {
-constexpr int THREADS = 512, WARPS = THREADS / 32;
+#ifndef KP_THREADS
+#define KP_THREADS 512
+#endif
+constexpr int THREADS = KP_THREADS, WARPS = THREADS / 32;
 constexpr int S = 1 << 16, HALF = 1 << 15, QL = HALF / 4;   // states, per CTA, quads per CTA
-constexpr int QPT = QL / THREADS;                            // 16 quads per thread
-constexpr uint32_t REMOTE_BYTES = 4 * THREADS * 16 + WARPS * 4;
+constexpr int QPT = QL / THREADS;                            // quads per thread (16 at 512 threads)
+constexpr int SPC = QPT / 4;                                 // slots (quads) per chunk: 4 chunks per thread
+constexpr uint32_t REMOTE_BYTES = SPC * THREADS * 16 + WARPS * 4;   // pair sums (32 KiB) + partials
 struct Smem {
     float recv[2][2][QL];           // [slot][source CTA][local q]: pair sums
-    float4 estage[2][4][THREADS];   // the own chunks' emissions of the next step (cp.async)
+    float4 estage[2][SPC][THREADS];   // the own chunks' emissions of the next step (cp.async)
     float part[2][2][WARPS];        // [slot][source CTA][warp]: partial sums of alpha
     uint64_t bar[2];
 };
@@ -247,18 +251,18 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
 }
 // chunk V: alpha_t from alpha_{t-1}, the received pair sums and the emissions
 template <int V>
-__device__ __forceinline__ void step_chunk(float4 (&a)[QPT], const float4 (&e)[4], const float* r0, const float* r1,
+__device__ __forceinline__ void step_chunk(float4 (&a)[QPT], const float4 (&e)[SPC], const float* r0, const float* r1,
                                            int tid, float inv, float p_stay, float p_step) {
-    float x[4], y[4];
+    float x[SPC], y[SPC];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        x[k] = r0[(4 * V + k) * THREADS + tid];
-        y[k] = r1[(4 * V + k) * THREADS + tid];
+    for (int k = 0; k < SPC; ++k) {
+        x[k] = r0[(SPC * V + k) * THREADS + tid];
+        y[k] = r1[(SPC * V + k) * THREADS + tid];
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < SPC; ++k) {
         const float st = p_step * (x[k] + y[k]);
-        float4& v = a[4 * V + k];
+        float4& v = a[SPC * V + k];
         v.x = inv * e[k].x * fmaf(p_stay, v.x, st);
         v.y = inv * e[k].y * fmaf(p_stay, v.y, st);
         v.z = inv * e[k].z * fmaf(p_stay, v.z, st);
@@ -266,28 +270,28 @@ __device__ __forceinline__ void step_chunk(float4 (&a)[QPT], const float4 (&e)[4
     }
 }
 template <int V>
-__device__ __forceinline__ void first_chunk(float4 (&a)[QPT], const float4 (&e)[4], float inv) {
+__device__ __forceinline__ void first_chunk(float4 (&a)[QPT], const float4 (&e)[SPC], float inv) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-        a[4 * V + k] = make_float4(inv * e[k].x, inv * e[k].y, inv * e[k].z, inv * e[k].w);
+    for (int k = 0; k < SPC; ++k)
+        a[SPC * V + k] = make_float4(inv * e[k].x, inv * e[k].y, inv * e[k].z, inv * e[k].w);
 }
 template <int V>
-__device__ __forceinline__ void load_chunk(float4 (&e)[4], const float4* row, int tid) {
+__device__ __forceinline__ void load_chunk(float4 (&e)[SPC], const float4* row, int tid) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) e[k] = ld_e4(row + (4 * V + k) * THREADS + tid);
+    for (int k = 0; k < SPC; ++k) e[k] = ld_e4(row + (SPC * V + k) * THREADS + tid);
 }
 template <int V>
 __device__ __forceinline__ void stage_chunk(float4 (*stage)[THREADS], const float4* row, int tid) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < SPC; ++k) {
         const uint32_t d = tc::smem_u32(&stage[k][tid]);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(row + (4 * V + k) * THREADS + tid)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(row + (SPC * V + k) * THREADS + tid)
                      : "memory");
     }
 }
-__device__ __forceinline__ void unstage(float4 (&e)[4], float4 (*stage)[THREADS], int tid) {
+__device__ __forceinline__ void unstage(float4 (&e)[SPC], float4 (*stage)[THREADS], int tid) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) e[k] = stage[k][tid];
+    for (int k = 0; k < SPC; ++k) e[k] = stage[k][tid];
 }
 // pair sums for target CTA R (chunks R and R + 2): float4s 512 k + t of R's buffer; returns their sum
 template <int R, bool REMOTE>
@@ -295,8 +299,8 @@ __device__ __forceinline__ float send_pairs(const float4 (&a)[QPT], float* own_s
                                             uint32_t remote_bar, int tid) {
     float part = 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const float4 v = add4(a[4 * R + k], a[4 * (R + 2) + k]);
+    for (int k = 0; k < SPC; ++k) {
+        const float4 v = add4(a[SPC * R + k], a[SPC * (R + 2) + k]);
         const int idx = 4 * (k * THREADS + tid);
         if (REMOTE) st_async_v4(remote_slot + 4u * idx, v, remote_bar);
         else *reinterpret_cast<float4*>(own_slot + idx) = v;
@@ -319,7 +323,7 @@ __device__ __forceinline__ void pair_run(Smem& sm, float p_stay, float p_step, c
     const int64_t ncl = gridDim.x >> 1;
     const float4* Erank = reinterpret_cast<const float4*>(E_lin + (size_t)R * HALF);
     float4 a[QPT];
-    float4 eP0[4], eP1[4];     // emissions of the peer-bound chunks P, P + 2 (registers)
+    float4 eP0[SPC], eP1[SPC];   // emissions of the peer-bound chunks P, P + 2 (registers)
     uint32_t g = 0;            // step counter across signals (slot and barrier phase)
     double ll = 0.0;
     int64_t prev = -1;
@@ -343,7 +347,9 @@ __device__ __forceinline__ void pair_run(Smem& sm, float p_stay, float p_step, c
             if (g > 0) {
                 tc::mbar_wait(&sm.bar[ps], ((g - 1) >> 1) & 1u);
                 if (tid == 0) expect_tx(&sm.bar[ps], REMOTE_BYTES);   // re-arm for step g + 1's bytes
-                float c = sm.part[ps][lane >> 4][lane & 15];
+                float c = 0.f;
+#pragma unroll
+                for (int w = lane; w < 2 * WARPS; w += 32) c += sm.part[ps][w / WARPS][w % WARPS];
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
                 if (R == 0 && tid == 0) {
@@ -368,7 +374,7 @@ __device__ __forceinline__ void pair_run(Smem& sm, float p_stay, float p_step, c
             float part = send_pairs<P, true>(a, own, rslot, rbar, tid);
             // own chunks (emissions staged in shared memory by the previous step)
             asm volatile("cp.async.wait_group 0;" ::: "memory");
-            float4 e0[4];
+            float4 e0[SPC];
             unstage(e0, sm.estage[0], tid);
             if (t == 0) first_chunk<R>(a, e0, inv);
             else step_chunk<R>(a, e0, r0, r1, tid, inv, p_stay, p_step);
@@ -401,7 +407,9 @@ __device__ __forceinline__ void pair_run(Smem& sm, float p_stay, float p_step, c
     if (g > 0) {   // the last step's c
         const uint32_t ps = (g - 1) & 1u;
         tc::mbar_wait(&sm.bar[ps], ((g - 1) >> 1) & 1u);
-        float c = sm.part[ps][lane >> 4][lane & 15];
+        float c = 0.f;
+#pragma unroll
+        for (int w = lane; w < 2 * WARPS; w += 32) c += sm.part[ps][w / WARPS][w % WARPS];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
         if (R == 0 && tid == 0) out_ll[prev] = ll + log_scale((double)c);

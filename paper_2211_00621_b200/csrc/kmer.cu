@@ -477,11 +477,8 @@ int pmx_hmm_kmer_forward_f32(int32_t kmer, float p_stay, float p_step, const flo
         if (kmer == 8 && !old && !vec) {
             // CTA pairs, alpha in registers: one signal per cluster at a time
             const size_t psm = sizeof(kp::Smem);
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_kmer_fwd_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
-                attr = true;
-            }
+            // per call: the attribute is per device (one process may drive several)
+            cudaFuncSetAttribute(k_kmer_fwd_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
             const int64_t clusters = nsig < sm_count() / 2 ? nsig : sm_count() / 2;
             k_kmer_fwd_pair<<<(unsigned)(2 * clusters), kp::THREADS, psm, st>>>(p_stay, p_step, E_lin, obs, nsig, T,
                                                                                  out_ll);
